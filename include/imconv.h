@@ -1,0 +1,163 @@
+/*
+ * imconv.h -- C ABI of the B200 (sm_100a) blocked implicit-im2col convolution.
+ *
+ * This is the drop-in boundary for the reference's kernel plug-in surface
+ * (/root/reference/pkg/src/sasim/_kernels/__init__.py).  Every entry point
+ * takes plain pointers and sizes; device pointers are CUDA global-memory
+ * addresses, `stream` is a cudaStream_t (NULL = legacy default stream).
+ * All calls are stream-ordered, re-entrant and keep no global mutable state
+ * other than a mutex-guarded, read-mostly cache of the driver entry point.
+ *
+ * Return codes: 0 on success, negative IMCONV_E* on argument errors,
+ * positive values are cudaError_t / CUresult codes from the runtime/driver.
+ * There is no CPU fallback: a missing GPU is an error (IMCONV_ENODEV).
+ */
+#ifndef IMCONV_H_
+#define IMCONV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IMCONV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define IMCONV_API __attribute__((visibility("default")))
+#else
+#define IMCONV_API
+#endif
+
+/* error codes (negative) */
+#define IMCONV_OK 0
+#define IMCONV_EINVAL -1     /* invalid spec / null pointer / bad extent          */
+#define IMCONV_EDTYPE -2     /* unsupported (in, out) dtype combination           */
+#define IMCONV_EALIGN -3     /* pointer not 16-byte aligned                       */
+#define IMCONV_ECHAN -4      /* C*elem or K*elem not a multiple of 16 bytes        */
+#define IMCONV_ETMAP -5      /* cuTensorMapEncode* rejected the operand            */
+#define IMCONV_ENODEV -6     /* no CUDA device / driver entry point unavailable    */
+#define IMCONV_ERANGE -7     /* extent exceeds a TMA limit (corner/offset/dim)     */
+
+/* element types */
+#define IMCONV_BF16 0
+#define IMCONV_F16 1
+#define IMCONV_I8 2
+#define IMCONV_F32 3
+#define IMCONV_I32 4
+
+/* scheduler order of the k-subtiles inside one output block
+ * (blocksched.py:25-30, :83-99) */
+#define IMCONV_ORDER_REUSE_AWARE 0  /* channel chunk outer, filter tap inner (default) */
+#define IMCONV_ORDER_FILTER_MAJOR 1 /* filter tap outer, channel chunk inner          */
+
+/*
+ * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,
+ * zero padding (virtual) and dilation per axis.
+ *
+ * Replaces: sasim._kernels.conv2d_nhwc(x, w, sh, sw, ph, pw, dh, dw)
+ *           (/root/reference/pkg/src/sasim/_kernels/__init__.py:37-46,
+ *            _native.pyx:20-47, _fallback.py:17-42),
+ *           and therefore core.direct_conv (core.py:194-208).
+ * Semantics: y[n,p,q,k] = sum_{r,s,c} x[n, p*sh + r*dh - ph, q*sw + s*dw - pw, c]
+ *                                   * w[r, s, c, k], out-of-range reads are 0.
+ * The lowered (n*p*q, r*s*c) matrix is never materialised: operands are
+ * produced by TMA im2col tensor maps straight into shared memory and
+ * contracted by tcgen05.mma with the accumulator in tensor memory.
+ *
+ * Layout: x (n,h,w,c) contiguous, w (r,s,c,k) contiguous, y (n,p,q,k)
+ * contiguous, caller-allocated (p, q from imconv_out_extent).
+ * dtypes: in = BF16/F16 -> out = BF16/F16/F32 (fp32 accumulation);
+ *         in = I8 -> out = I32 (int32 accumulation, bit-exact).
+ * Requires c*elem % 16 == 0 and k*elem % 16 == 0 (the Python shim pads).
+ * tile_n: 0 = auto, else 64/128/256 (output channels per CTA tile).
+ * num_ctas: 0 = one persistent CTA per SM, else the grid size.
+ */
+typedef struct imconv_conv_args {
+    const void *x;
+    const void *w;
+    void *y;
+    int32_t in_dtype;
+    int32_t out_dtype;
+    int64_t n, h, w_, c;   /* input extents (w_ = width) */
+    int64_t k, r, s;       /* output channels, filter rows, filter cols */
+    int32_t stride_h, stride_w;
+    int32_t pad_h, pad_w;
+    int32_t dil_h, dil_w;
+    int32_t tile_n;
+    int32_t num_ctas;
+    int32_t order;         /* IMCONV_ORDER_* */
+    int32_t reserved;
+} imconv_conv_args;
+
+IMCONV_API int imconv_conv2d_nhwc(const imconv_conv_args *args, void *stream);
+
+/* Output extent, core.py:89-95: (size + 2*pad - dil*(f-1) - 1)/stride + 1
+ * (returns <= 0 when the effective filter exceeds the padded input). */
+IMCONV_API int64_t imconv_out_extent(int64_t size, int64_t f, int64_t stride, int64_t pad, int64_t dil);
+
+/*
+ * C = A @ B, row-major A (m, kd) and B (kd, n), through the same tcgen05
+ * kernel (a 1x1 stride-1 convolution over an (1, 1, m, kd) "image").
+ * Replaces: core.gemm (core.py:211-218) on the explicit-lowering path
+ * (simulator.py:527-532, lowering.py:98-122).
+ */
+IMCONV_API int imconv_gemm(const void *a, const void *b, void *c, int32_t in_dtype, int32_t out_dtype,
+                int64_t m, int64_t kd, int64_t n, void *stream);
+
+/*
+ * One decomposed 1x1 tile's gather, (n*ho*wo, c) row-major, zero rows at
+ * padding.  Replaces _kernels.tile_gather_nhwc (__init__.py:49-50,
+ * _native.pyx:50-69) used by TileDescriptor.gather_matrix (lowering.py:88-95).
+ * elem_bytes in {1,2,4,8}.
+ */
+IMCONV_API int imconv_tile_gather_nhwc(const void *x, void *out, int32_t elem_bytes,
+                            int64_t n, int64_t h, int64_t w_, int64_t c,
+                            int32_t r, int32_t s, int32_t stride_h, int32_t stride_w,
+                            int32_t pad_h, int32_t pad_w, int32_t dil_h, int32_t dil_w,
+                            int64_t ho, int64_t wo, void *stream);
+
+/*
+ * Explicit im2col, (n*ho*wo, hf*wf*c) row-major; column order channel-first
+ * (r*wf + s)*c + ch or channel-last (ch*hf + r)*wf + s.
+ * Replaces _kernels.im2col_nhwc (__init__.py:53-54, _native.pyx:72-99) and
+ * lowering.im2col_explicit (lowering.py:98-110).  This is the K3 kernel of
+ * the explicit-overhead measurement; it writes the lowered matrix to HBM.
+ */
+IMCONV_API int imconv_im2col_nhwc(const void *x, void *out, int32_t elem_bytes,
+                       int64_t n, int64_t h, int64_t w_, int64_t c,
+                       int32_t hf, int32_t wf, int32_t stride_h, int32_t stride_w,
+                       int32_t pad_h, int32_t pad_w, int32_t dil_h, int32_t dil_w,
+                       int32_t channel_first, void *stream);
+
+/*
+ * Zero-padding copy (outer, c, d) -> (outer, c_pad, d_pad), elem_bytes in
+ * {1,2,4}; used by the Python shim to meet the 16-byte channel alignment
+ * (exact: padded channels/filters are zero).  Device pointers.
+ */
+IMCONV_API int imconv_pad_copy(const void *src, void *dst, int32_t elem_bytes, int64_t outer,
+                    int64_t c, int64_t d, int64_t c_pad, int64_t d_pad, void *stream);
+
+/*
+ * Fully-associative LRU replay of an int64 key stream (host memory, host
+ * code).  Replaces _kernels.lru_simulate (__init__.py:57-59,
+ * _native.pyx:102-149) behind blocksched.reuse_traffic (blocksched.py:131-151).
+ */
+IMCONV_API int imconv_lru_simulate(const int64_t *keys, int64_t count, int64_t capacity,
+                        int64_t *hits, int64_t *misses);
+
+/* Device / build introspection (no compute). */
+IMCONV_API int imconv_abi_version(void);
+IMCONV_API int imconv_device_sm_count(int32_t *sm_count);
+IMCONV_API const char *imconv_strerror(int code);
+
+/* Number of kernel launches issued by this library on the calling thread
+ * since the last reset (instrumentation for bench.py's gpu_launches). */
+IMCONV_API int64_t imconv_launch_count(void);
+IMCONV_API void imconv_reset_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IMCONV_H_ */

@@ -1,0 +1,50 @@
+"""Build the sm_100a extension in-tree: paper_2110_03901_b200/libimconv.so.
+
+Plain nvcc (no torch JIT cache): the shared object lives next to the package
+so it travels to the GPU box with the repo snapshot.  cudart is linked
+statically and libcuda is resolved at run time through
+cudaGetDriverEntryPoint, so the library loads (and exports every symbol of
+include/imconv.h) on a machine without a GPU.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libimconv.so")
+SOURCES = [os.path.join(CSRC, f) for f in ("imconv_api.cu", "lru.cpp")]
+HEADERS = [os.path.join(CSRC, f) for f in ("ptx.cuh", "conv_kernel.cuh", "aux_kernels.cuh")] + [
+    os.path.join(ROOT, "include", "imconv.h")]
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+         "--expt-relaxed-constexpr", "-cudart", "static"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    cmd = [NVCC] + ARCH + FLAGS + ["-I", os.path.join(ROOT, "include"), "-shared", "-o", LIB] + SOURCES
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force=True, verbose="-v" in sys.argv)
+    print(LIB)

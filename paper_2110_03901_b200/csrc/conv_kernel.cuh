@@ -1,0 +1,357 @@
+// conv_kernel.cuh -- the blocked channel-first implicit-im2col convolution
+// (arXiv 2110.03901 §5) as a persistent, warp-specialised tcgen05 kernel.
+//
+// GEMM view: row m = (n*P + p)*Q + q of the output,
+// reduction index k = (r*S + s)*C + c (channel-first), B = HWCN filter
+// reshaped to (R*S*C, K).  The lowered matrix is never materialised: for
+// every (output block, k-subtile) the TMA engine gathers the block's 128
+// output pixels for one filter tap <r,s> and one channel chunk straight from
+// the NHWC tensor into a swizzled shared-memory tile (im2col mode: the base
+// pixel is (q*sw - pw, p*sh - ph) and the tap enters as the im2col offset
+// (s*dw, r*dh); out-of-image pixels are zero-filled by the hardware, which is
+// the reference's "virtual padding", lowering.py:59-64).
+//
+// Warp roles (256 threads, one CTA per SM, persistent over output blocks):
+//   warp 0      : TMA producer (one elected lane)       -- operand generation
+//   warp 1      : tcgen05.mma issuer (one elected lane) -- contraction into TMEM
+//   warp 2      : TMEM allocator
+//   warps 4..7  : epilogue, TMEM -> registers -> NHWC global stores
+// Pipelines: STAGES-deep smem ring (full/empty mbarriers, TMA complete_tx and
+// tcgen05.commit), and a 2-deep TMEM accumulator ring (tfull/tempty) so the
+// epilogue of block i overlaps the main loop of block i+1.
+//
+// k-subtile order inside a block follows blocksched.order_subtiles
+// (blocksched.py:83-99): REUSE_AWARE = channel chunk outer / tap inner (the
+// paper's reordering, consecutive taps re-read ~(S-1)/S of the same input
+// window from L1/L2); FILTER_MAJOR = tap outer.  Blocks are rasterised
+// m-major with the n-blocks of one m-block adjacent in the schedule, so the
+// CTAs working on one input window at the same time share it through L2.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "ptx.cuh"
+
+namespace imconv {
+
+constexpr int kBM = 128;           // output pixels per block (MMA M)
+constexpr int kRowBytes = 128;     // bytes of reduction per stage per row (one 128B swizzle span)
+constexpr int kAStage = kBM * kRowBytes;  // 16 KiB of A per stage
+constexpr int kThreads = 256;
+
+enum ElemKind : int { ELEM_BF16 = 0, ELEM_F16 = 1, ELEM_I8 = 2 };
+enum OutKind : int { OUT_BF16 = 0, OUT_F16 = 1, OUT_F32 = 2, OUT_I32 = 3 };
+enum ALayout : int { A_NONE = 0, A_SW32 = 1, A_SW64 = 2, A_SW128 = 3 };
+
+struct ConvParams {
+    int n, h, w, c;      // input extents (c as stored, 16-byte aligned)
+    int k;               // output channels (as stored in y)
+    int r, s;            // filter
+    int sh, sw, ph, pw, dh, dw;
+    int p, q;            // output spatial extents
+    long long m;         // n*p*q
+    int m_tiles, n_tiles;
+    int rs;              // r*s
+    int tps;             // filter taps per pipeline stage (1 when c*elem >= 128)
+    int c_chunks;        // channel chunks per tap (tps == 1)
+    int k_stages;        // pipeline stages per output block
+    int a_layout;        // ALayout of the A tile
+    int order;           // 0 reuse-aware, 1 filter-major
+    void *y;
+    long long ldy;       // = k
+};
+
+template <int ELEM>
+struct ElemTraits;
+template <>
+struct ElemTraits<ELEM_BF16> {
+    static constexpr int kBytes = 2;
+    static constexpr uint32_t kFmt = 1;  // BF16
+};
+template <>
+struct ElemTraits<ELEM_F16> {
+    static constexpr int kBytes = 2;
+    static constexpr uint32_t kFmt = 0;  // F16
+};
+template <>
+struct ElemTraits<ELEM_I8> {
+    static constexpr int kBytes = 1;
+    static constexpr uint32_t kFmt = 1;  // signed 8-bit
+};
+
+// tcgen05 instruction descriptor: A K-major, B MN-major (HWCN filter rows
+// are contiguous over the output channel), M = 128, N = BN.
+template <int ELEM, int BN>
+__device__ __forceinline__ uint32_t make_idesc() {
+    uint32_t d = 0;
+    d |= (ELEM == ELEM_I8 ? 2u : 1u) << 4;          // D format: S32 / F32
+    d |= ElemTraits<ELEM>::kFmt << 7;               // A format
+    d |= ElemTraits<ELEM>::kFmt << 10;              // B format
+    d |= 0u << 15;                                  // A major: K
+    d |= 1u << 16;                                  // B major: MN
+    d |= static_cast<uint32_t>(BN >> 3) << 17;      // N
+    d |= static_cast<uint32_t>(kBM >> 4) << 24;     // M
+    return d;
+}
+
+template <int OUT>
+__device__ __forceinline__ void store_row_chunk(const ConvParams &p, long long m, int col0, const uint32_t (&v)[32]) {
+    if constexpr (OUT == OUT_BF16 || OUT == OUT_F16) {
+        using T = typename std::conditional<OUT == OUT_BF16, __nv_bfloat16, __half>::type;
+        T *row = reinterpret_cast<T *>(p.y) + m * p.ldy;
+        if (col0 + 32 <= p.k && (p.k & 7) == 0) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
+                if constexpr (OUT == OUT_BF16) {
+                    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+                    packed[i] = *reinterpret_cast<uint32_t *>(&t);
+                } else {
+                    __half2 t = __floats2half2_rn(a, b);
+                    packed[i] = *reinterpret_cast<uint32_t *>(&t);
+                }
+            }
+            uint4 *dst = reinterpret_cast<uint4 *>(row + col0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (col0 + i < p.k) {
+                    if constexpr (OUT == OUT_BF16)
+                        row[col0 + i] = __float2bfloat16_rn(__uint_as_float(v[i]));
+                    else
+                        row[col0 + i] = __float2half_rn(__uint_as_float(v[i]));
+                }
+            }
+        }
+    } else {
+        // fp32 or int32: raw 32-bit accumulator words
+        uint32_t *row = reinterpret_cast<uint32_t *>(p.y) + m * p.ldy;
+        if (col0 + 32 <= p.k && (p.k & 3) == 0) {
+            uint4 *dst = reinterpret_cast<uint4 *>(row + col0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (col0 + i < p.k) row[col0 + i] = v[i];
+        }
+    }
+}
+
+template <int ELEM, int OUT, int BN, int STAGES>
+struct ConvCfg {
+    static constexpr int kE = ElemTraits<ELEM>::kBytes;
+    static constexpr int kBKE = kRowBytes / kE;      // reduction elements per stage
+    static constexpr int kNC = kRowBytes / kE;       // n-chunk of one MN-major SW128 atom column
+    static constexpr int kBStage = BN * kRowBytes;   // bytes of B per stage
+    static constexpr int kMmaK = 32 / kE;            // reduction elements per tcgen05.mma
+    static constexpr int kMmaPerStage = kBKE / kMmaK;  // = 4
+    static constexpr int kTmemCols = 2 * BN;         // double-buffered accumulator
+    static constexpr int kSmemBytes = STAGES * (kAStage + kBStage) + 1024 /*align*/ + 256 /*barriers*/;
+    static_assert(BN % kNC == 0, "BN must be a multiple of the swizzle atom width");
+    static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
+};
+
+template <int ELEM, int OUT, int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                    const ConvParams p) {
+    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *smem_a = smem;
+    uint8_t *smem_b = smem + STAGES * kAStage;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_b + STAGES * Cfg::kBStage);
+    uint64_t *full = bars;
+    uint64_t *empty = bars + STAGES;
+    uint64_t *tfull = bars + 2 * STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const long long total_tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmap_a);
+        ptx::prefetch_tmap(&tmap_b);
+        for (int i = 0; i < STAGES; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 4);  // one arrival per epilogue warp
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer: operand generation =====================
+        if (lane == 0) {
+            const uint64_t pol_a = ptx::policy_evict_normal();
+            const uint64_t pol_b = ptx::policy_evict_last();  // filters are re-read by every block
+            const int pq = p.p * p.q;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+                const long long m_tile = tile / p.n_tiles;
+                const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
+                const long long m0 = m_tile * kBM;
+                const int n0 = static_cast<int>(m0 / pq);
+                const int rem = static_cast<int>(m0 - static_cast<long long>(n0) * pq);
+                const int p0 = rem / p.q;
+                const int q0 = rem - p0 * p.q;
+                const int w0 = q0 * p.sw - p.pw;  // base pixel (im2col bounding-box coordinates)
+                const int h0 = p0 * p.sh - p.ph;
+                const int nb0 = n_tile * BN;
+                for (int kb = 0; kb < p.k_stages; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], kAStage + Cfg::kBStage);
+                    uint8_t *a_dst = smem_a + stage * kAStage;
+                    uint8_t *b_dst = smem_b + stage * Cfg::kBStage;
+                    int brow;
+                    if (p.tps == 1) {
+                        int chunk, tap;
+                        if (p.order == 0) {
+                            chunk = kb / p.rs;
+                            tap = kb - chunk * p.rs;
+                        } else {
+                            tap = kb / p.c_chunks;
+                            chunk = kb - tap * p.c_chunks;
+                        }
+                        const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
+                        const int c0 = chunk * Cfg::kBKE;
+                        ptx::tma_load_im2col_4d(a_dst, &tmap_a, &full[stage], c0, w0, h0, n0,
+                                                static_cast<uint16_t>(s * p.dw), static_cast<uint16_t>(r * p.dh),
+                                                pol_a);
+                        brow = tap * p.c + c0;
+                    } else {
+                        // small-C layers: pack tps taps side by side along the
+                        // reduction (the paper's multi-tile packing, §4.2)
+                        const int tap0 = kb * p.tps;
+                        const int blk = kAStage / p.tps;
+                        for (int t = 0; t < p.tps; ++t) {
+                            const int tap = min(tap0 + t, p.rs - 1);  // past-the-end taps meet zero filter rows
+                            const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
+                            ptx::tma_load_im2col_4d(a_dst + t * blk, &tmap_a, &full[stage], 0, w0, h0, n0,
+                                                    static_cast<uint16_t>(s * p.dw),
+                                                    static_cast<uint16_t>(r * p.dh), pol_a);
+                        }
+                        brow = tap0 * p.c;
+                    }
+#pragma unroll
+                    for (int j = 0; j < BN / Cfg::kNC; ++j)
+                        ptx::tma_load_2d(b_dst + j * (Cfg::kBKE * kRowBytes), &tmap_b, &full[stage],
+                                         nb0 + j * Cfg::kNC, brow, pol_b);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ===================== tcgen05 MMA issuer =====================
+        const uint32_t idesc = make_idesc<ELEM, BN>();
+        uint32_t a_lbo, a_sbo, a_layout;
+        switch (p.a_layout) {
+            case A_SW128: a_lbo = 16; a_sbo = 1024; a_layout = ptx::LAYOUT_SW128; break;
+            case A_SW64: a_lbo = 16; a_sbo = 512; a_layout = ptx::LAYOUT_SW64; break;
+            case A_SW32: a_lbo = 16; a_sbo = 256; a_layout = ptx::LAYOUT_SW32; break;
+            default: a_lbo = kBM * 16; a_sbo = 128; a_layout = ptx::LAYOUT_NONE; break;
+        }
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+            for (int kb = 0; kb < p.k_stages; ++kb) {
+                ptx::mbar_wait(&full[stage], phase);
+                ptx::tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a_base = ptx::smem_u32(smem_a + stage * kAStage);
+                    const uint32_t b_base = ptx::smem_u32(smem_b + stage * Cfg::kBStage);
+#pragma unroll
+                    for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk) {
+                        uint32_t a_off;
+                        switch (p.a_layout) {
+                            case A_SW128: a_off = kk * 32; break;
+                            case A_SW64: a_off = (kk >> 1) * (kBM * 64) + (kk & 1) * 32; break;
+                            case A_SW32: a_off = kk * (kBM * 32); break;
+                            default: a_off = kk * 2 * (kBM * 16); break;
+                        }
+                        const uint64_t adesc = ptx::smem_desc(a_base + a_off, a_lbo, a_sbo, a_layout);
+                        const uint64_t bdesc = ptx::smem_desc(b_base + kk * (Cfg::kMmaK * kRowBytes),
+                                                              Cfg::kBKE * kRowBytes, 1024, ptx::LAYOUT_SW128);
+                        const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
+                        if constexpr (ELEM == ELEM_I8)
+                            ptx::mma_i8(d_tmem, adesc, bdesc, idesc, accum);
+                        else
+                            ptx::mma_f16(d_tmem, adesc, bdesc, idesc, accum);
+                    }
+                    ptx::mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (lane == 0) ptx::mma_commit(&tfull[acc]);  // accumulator complete -> epilogue
+            __syncwarp();
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue: TMEM -> registers -> NHWC =====================
+        const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+            const long long m_tile = tile / p.n_tiles;
+            const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
+            const long long m = m_tile * kBM + quarter * 32 + lane;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int j = 0; j < BN / 32; ++j) {
+                uint32_t v[32];
+                const uint32_t taddr =
+                    tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + j * 32);
+                ptx::tmem_ld_32x32b_x32(taddr, v);
+                ptx::tmem_ld_wait();
+                const int col0 = n_tile * BN + j * 32;
+                if (m < p.m && col0 < p.k) store_row_chunk<OUT>(p, m, col0, v);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    }
+}
+
+}  // namespace imconv

@@ -1,0 +1,407 @@
+// imconv_api.cu -- C ABI (include/imconv.h) over the sm_100a kernels.
+//
+// Host-side responsibilities: validate the spec (the reference validates in
+// ConvSpec.__post_init__, core.py:72-87, and _as_nhwc/_as_filter_hwcn,
+// core.py:178-191), encode the TMA tensor maps (im2col map for the NHWC
+// activations, tiled map for the HWCN filter), choose the block shape, and
+// launch the persistent kernel on the caller's stream.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+
+#include "../../include/imconv.h"
+#include "aux_kernels.cuh"
+#include "conv_kernel.cuh"
+
+namespace imconv {
+namespace {
+
+thread_local int64_t g_launches = 0;
+
+std::mutex g_mu;
+PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
+int g_driver_version = 0;
+int g_sm_count[64] = {0};
+
+int load_driver_entry_points() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_encode_im2col && g_encode_tiled) return 0;
+    cudaDriverEntryPointQueryResult q1, q2;
+    void *f1 = nullptr, *f2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f1, cudaEnableDefault, &q1) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess || f1 == nullptr)
+        return IMCONV_ENODEV;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f2, cudaEnableDefault, &q2) != cudaSuccess ||
+        q2 != cudaDriverEntryPointSuccess || f2 == nullptr)
+        return IMCONV_ENODEV;
+    cudaDriverGetVersion(&g_driver_version);
+    g_encode_im2col = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(f1);
+    g_encode_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f2);
+    return 0;
+}
+
+int sm_count_for_current_device(int *out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return IMCONV_ENODEV;
+    if (dev >= 0 && dev < 64 && g_sm_count[dev] > 0) {
+        *out = g_sm_count[dev];
+        return 0;
+    }
+    int n = 0;
+    e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess || n <= 0) return IMCONV_ENODEV;
+    if (dev >= 0 && dev < 64) g_sm_count[dev] = n;
+    *out = n;
+    return 0;
+}
+
+inline int64_t out_extent(int64_t size, int64_t f, int64_t stride, int64_t pad, int64_t dil) {
+    return (size + 2 * pad - dil * (f - 1) - 1) / stride + 1;
+}
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+CUtensorMapDataType tmap_dtype(int in_dtype) {
+    switch (in_dtype) {
+        case IMCONV_BF16: return CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        case IMCONV_F16: return CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+        default: return CU_TENSOR_MAP_DATA_TYPE_UINT8;  // int8 bytes; zero fill is 0 either way
+    }
+}
+
+int elem_bytes(int in_dtype) { return in_dtype == IMCONV_I8 ? 1 : 2; }
+
+template <int ELEM, int OUT, int BN, int STAGES>
+int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvParams &p, int grid, cudaStream_t st) {
+    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES>;
+    auto kern = conv_fwd_kernel<ELEM, OUT, BN, STAGES>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    });
+    if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
+    kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(ta, tb, p);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+// BN -> pipeline depth that fits ~200 KB of shared memory.
+template <int ELEM, int OUT>
+int dispatch_bn(int bn, const CUtensorMap &ta, const CUtensorMap &tb, const ConvParams &p, int grid,
+                cudaStream_t st) {
+    if constexpr (ELEM == ELEM_I8) {
+        if (bn == 128) return launch_conv<ELEM, OUT, 128, 6>(ta, tb, p, grid, st);
+        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4>(ta, tb, p, grid, st);
+    } else {
+        if (bn == 64) return launch_conv<ELEM, OUT, 64, 8>(ta, tb, p, grid, st);
+        if (bn == 128) return launch_conv<ELEM, OUT, 128, 6>(ta, tb, p, grid, st);
+        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4>(ta, tb, p, grid, st);
+    }
+    return IMCONV_EINVAL;
+}
+
+int pick_bn(int in_dtype, int64_t k, int requested) {
+    const int nc = in_dtype == IMCONV_I8 ? 128 : 64;
+    if (requested != 0) {
+        if (requested % nc != 0 || requested > 256 || requested < nc) return -1;
+        return requested;
+    }
+    int64_t bn = ((k + nc - 1) / nc) * nc;
+    if (bn > 256) bn = 256;
+    return static_cast<int>(bn);
+}
+
+}  // namespace
+}  // namespace imconv
+
+using namespace imconv;
+
+extern "C" {
+
+int imconv_abi_version(void) { return IMCONV_ABI_VERSION; }
+
+int64_t imconv_out_extent(int64_t size, int64_t f, int64_t stride, int64_t pad, int64_t dil) {
+    if (stride < 1 || dil < 1 || f < 1 || pad < 0) return 0;
+    const int64_t ext = dil * (f - 1) + 1;
+    if (ext > size + 2 * pad) return 0;
+    return out_extent(size, f, stride, pad, dil);
+}
+
+const char *imconv_strerror(int code) {
+    switch (code) {
+        case IMCONV_OK: return "ok";
+        case IMCONV_EINVAL: return "invalid argument (spec, extent or null pointer)";
+        case IMCONV_EDTYPE: return "unsupported dtype combination";
+        case IMCONV_EALIGN: return "pointer is not 16-byte aligned";
+        case IMCONV_ECHAN: return "channel count times element size must be a multiple of 16 bytes";
+        case IMCONV_ETMAP: return "TMA tensor-map encoding rejected the operand";
+        case IMCONV_ENODEV: return "no CUDA device or driver entry point";
+        case IMCONV_ERANGE: return "extent exceeds a TMA im2col limit";
+        default: break;
+    }
+    if (code > 0) return cudaGetErrorString(static_cast<cudaError_t>(code));
+    return "unknown error";
+}
+
+int imconv_device_sm_count(int32_t *sm_count) {
+    if (!sm_count) return IMCONV_EINVAL;
+    int n = 0;
+    int rc = sm_count_for_current_device(&n);
+    if (rc) return rc;
+    *sm_count = n;
+    return 0;
+}
+
+int64_t imconv_launch_count(void) { return g_launches; }
+void imconv_reset_launch_count(void) { g_launches = 0; }
+
+int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
+    if (!a || !a->x || !a->w || !a->y) return IMCONV_EINVAL;
+    const int64_t N = a->n, H = a->h, W = a->w_, C = a->c, K = a->k, R = a->r, S = a->s;
+    if (N < 1 || H < 1 || W < 1 || C < 1 || K < 1 || R < 1 || S < 1) return IMCONV_EINVAL;
+    if (a->stride_h < 1 || a->stride_w < 1 || a->dil_h < 1 || a->dil_w < 1 || a->pad_h < 0 || a->pad_w < 0)
+        return IMCONV_EINVAL;
+    const int64_t P = imconv_out_extent(H, R, a->stride_h, a->pad_h, a->dil_h);
+    const int64_t Q = imconv_out_extent(W, S, a->stride_w, a->pad_w, a->dil_w);
+    if (P < 1 || Q < 1) return IMCONV_EINVAL;
+
+    const bool f16in = a->in_dtype == IMCONV_BF16 || a->in_dtype == IMCONV_F16;
+    if (!(f16in && (a->out_dtype == a->in_dtype || a->out_dtype == IMCONV_F32)) &&
+        !(a->in_dtype == IMCONV_I8 && a->out_dtype == IMCONV_I32))
+        return IMCONV_EDTYPE;
+    const int E = elem_bytes(a->in_dtype);
+    if ((C * E) % 16 != 0 || (K * E) % 16 != 0) return IMCONV_ECHAN;
+    if (!aligned16(a->x) || !aligned16(a->w) || !aligned16(a->y)) return IMCONV_EALIGN;
+
+    // TMA im2col limits for a 4-D tensor: corners in [-128,127], tap offsets
+    // in [0,255], traversal stride <= 8, dims < 2^32.
+    const int64_t lo_w = -a->pad_w, lo_h = -a->pad_h;
+    const int64_t up_w = a->pad_w - static_cast<int64_t>(a->dil_w) * (S - 1);
+    const int64_t up_h = a->pad_h - static_cast<int64_t>(a->dil_h) * (R - 1);
+    if (lo_w < -128 || lo_h < -128 || up_w < -128 || up_h < -128 || up_w > 127 || up_h > 127) return IMCONV_ERANGE;
+    if (static_cast<int64_t>(a->dil_w) * (S - 1) > 255 || static_cast<int64_t>(a->dil_h) * (R - 1) > 255)
+        return IMCONV_ERANGE;
+    if (a->stride_h > 8 || a->stride_w > 8) return IMCONV_ERANGE;
+    const int64_t M = N * P * Q;
+    if (M >= (1ll << 40) || R * S * C >= (1ll << 31) || H * W >= (1ll << 31)) return IMCONV_ERANGE;
+
+    int rc = load_driver_entry_points();
+    if (rc) return rc;
+    int sms = 0;
+    rc = sm_count_for_current_device(&sms);
+    if (rc) return rc;
+
+    const int bn = pick_bn(a->in_dtype, K, a->tile_n);
+    if (bn < 0) return IMCONV_EINVAL;
+
+    // ---- A operand: im2col tensor map over NHWC ----
+    const int64_t cbytes = C * E;
+    const int row_bytes = cbytes >= 128 ? 128 : static_cast<int>(cbytes);  // 16, 32, 64 or 128
+    int a_layout;
+    CUtensorMapSwizzle a_swz;
+    switch (row_bytes) {
+        case 128: a_layout = A_SW128; a_swz = CU_TENSOR_MAP_SWIZZLE_128B; break;
+        case 64: a_layout = A_SW64; a_swz = CU_TENSOR_MAP_SWIZZLE_64B; break;
+        case 32: a_layout = A_SW32; a_swz = CU_TENSOR_MAP_SWIZZLE_32B; break;
+        case 16: a_layout = A_NONE; a_swz = CU_TENSOR_MAP_SWIZZLE_NONE; break;
+        default: return IMCONV_ECHAN;  // 48, 80, 96, 112 bytes: pad to the next power of two
+    }
+    const int tps = kRowBytes / row_bytes;
+
+    CUtensorMap ta, tb;
+    std::memset(&ta, 0, sizeof(ta));
+    std::memset(&tb, 0, sizeof(tb));
+    {
+        cuuint64_t gdim[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(N)};
+        cuuint64_t gstride[3] = {static_cast<cuuint64_t>(C * E), static_cast<cuuint64_t>(W * C * E),
+                                 static_cast<cuuint64_t>(H * W * C * E)};
+        int lower[2] = {static_cast<int>(lo_w), static_cast<int>(lo_h)};  // {W, H}
+        int upper[2] = {static_cast<int>(up_w), static_cast<int>(up_h)};
+        cuuint32_t estride[4] = {1, static_cast<cuuint32_t>(a->stride_w), static_cast<cuuint32_t>(a->stride_h), 1};
+        CUresult cr = g_encode_im2col(&ta, tmap_dtype(a->in_dtype), 4, const_cast<void *>(a->x), gdim, gstride,
+                                      lower, upper, static_cast<cuuint32_t>(row_bytes / E), kBM, estride,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, a_swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
+        // Same driver quirk CUTLASS works around for im2col maps over small
+        // tensors on drivers <= 13.1 (copy_traits_sm90_im2col.hpp).
+        if (g_driver_version <= 13010 && N * H * W * C * E < 131072)
+            reinterpret_cast<uint64_t *>(&ta)[1] &= ~(1ull << 21);
+    }
+    // ---- B operand: tiled map over the HWCN filter viewed as (R*S*C, K) ----
+    {
+        const int nc = kRowBytes / E;
+        cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(R * S * C)};
+        cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * E)};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(kRowBytes / E)};
+        cuuint32_t estride[2] = {1, 1};
+        CUresult cr = g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 2, const_cast<void *>(a->w), gdim, gstride, box,
+                                     estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
+    }
+
+    ConvParams p{};
+    p.n = static_cast<int>(N);
+    p.h = static_cast<int>(H);
+    p.w = static_cast<int>(W);
+    p.c = static_cast<int>(C);
+    p.k = static_cast<int>(K);
+    p.r = static_cast<int>(R);
+    p.s = static_cast<int>(S);
+    p.sh = a->stride_h;
+    p.sw = a->stride_w;
+    p.ph = a->pad_h;
+    p.pw = a->pad_w;
+    p.dh = a->dil_h;
+    p.dw = a->dil_w;
+    p.p = static_cast<int>(P);
+    p.q = static_cast<int>(Q);
+    p.m = M;
+    p.m_tiles = static_cast<int>((M + kBM - 1) / kBM);
+    p.n_tiles = static_cast<int>((K + bn - 1) / bn);
+    p.rs = static_cast<int>(R * S);
+    p.tps = tps;
+    p.c_chunks = tps == 1 ? static_cast<int>((cbytes + kRowBytes - 1) / kRowBytes) : 1;
+    p.k_stages = tps == 1 ? p.c_chunks * p.rs : (p.rs + tps - 1) / tps;
+    p.a_layout = a_layout;
+    p.order = a->order == IMCONV_ORDER_FILTER_MAJOR ? 1 : 0;
+    p.y = a->y;
+    p.ldy = K;
+
+    const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
+    int grid = a->num_ctas > 0 ? a->num_ctas : sms;
+    if (grid > tiles) grid = static_cast<int>(tiles);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+
+    switch (a->in_dtype) {
+        case IMCONV_BF16:
+            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, ta, tb, p, grid, st)
+                                              : dispatch_bn<ELEM_BF16, OUT_BF16>(bn, ta, tb, p, grid, st);
+        case IMCONV_F16:
+            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_F16, OUT_F32>(bn, ta, tb, p, grid, st)
+                                              : dispatch_bn<ELEM_F16, OUT_F16>(bn, ta, tb, p, grid, st);
+        case IMCONV_I8: return dispatch_bn<ELEM_I8, OUT_I32>(bn, ta, tb, p, grid, st);
+        default: return IMCONV_EDTYPE;
+    }
+}
+
+int imconv_gemm(const void *A, const void *B, void *Cm, int32_t in_dtype, int32_t out_dtype, int64_t m, int64_t kd,
+                int64_t n, void *stream) {
+    if (m < 1 || kd < 1 || n < 1) return IMCONV_EINVAL;
+    // A (m, kd) row-major is an NHWC image (1, 1, m, kd); B (kd, n) is an
+    // HWCN 1x1 filter; the 1x1 stride-1 convolution is exactly A @ B.
+    imconv_conv_args a{};
+    a.x = A;
+    a.w = B;
+    a.y = Cm;
+    a.in_dtype = in_dtype;
+    a.out_dtype = out_dtype;
+    a.n = 1;
+    a.h = 1;
+    a.w_ = m;
+    a.c = kd;
+    a.k = n;
+    a.r = 1;
+    a.s = 1;
+    a.stride_h = a.stride_w = 1;
+    a.dil_h = a.dil_w = 1;
+    return imconv_conv2d_nhwc(&a, stream);
+}
+
+static int grid_for(long long work) {
+    long long g = (work + 255) / 256;
+    if (g > 148LL * 16) g = 148LL * 16;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+
+static int launch_gather(const void *x, void *out, int32_t eb, int64_t n, int64_t h, int64_t w, int64_t c,
+                         int32_t hf, int32_t wf, int32_t r_fix, int32_t s_fix, int32_t sh, int32_t sw, int32_t ph,
+                         int32_t pw, int32_t dh, int32_t dw, int64_t ho, int64_t wo, int32_t channel_first,
+                         cudaStream_t st) {
+    const long long M = n * ho * wo;
+    const long long taps = r_fix >= 0 ? 1 : static_cast<long long>(hf) * wf;
+    if ((c * eb) % 16 == 0 && (channel_first || r_fix >= 0) && aligned16(x) && aligned16(out)) {
+        const int c_vec = static_cast<int>(c * eb / 16);
+        const long long work = M * taps * c_vec;
+        im2col_cf_vec16_kernel<<<grid_for(work), 256, 0, st>>>(
+            reinterpret_cast<const uint4 *>(x), reinterpret_cast<uint4 *>(out), M, static_cast<int>(h),
+            static_cast<int>(w), c_vec, static_cast<int>(ho), static_cast<int>(wo), r_fix, s_fix,
+            static_cast<int>(taps), wf, sh, sw, ph, pw, dh, dw);
+    } else {
+        const long long work = M * taps * c;
+#define IMCONV_GEN(T)                                                                                          \
+    im2col_generic_kernel<T><<<grid_for(work), 256, 0, st>>>(                                                   \
+        reinterpret_cast<const T *>(x), reinterpret_cast<T *>(out), M, static_cast<int>(h), static_cast<int>(w), \
+        static_cast<int>(c), static_cast<int>(ho), static_cast<int>(wo), hf, wf, sh, sw, ph, pw, dh, dw,        \
+        channel_first, r_fix, s_fix)
+        switch (eb) {
+            case 1: IMCONV_GEN(uint8_t); break;
+            case 2: IMCONV_GEN(uint16_t); break;
+            case 4: IMCONV_GEN(uint32_t); break;
+            case 8: IMCONV_GEN(unsigned long long); break;
+            default: return IMCONV_EDTYPE;
+        }
+#undef IMCONV_GEN
+    }
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+int imconv_tile_gather_nhwc(const void *x, void *out, int32_t elem_bytes_, int64_t n, int64_t h, int64_t w_,
+                            int64_t c, int32_t r, int32_t s, int32_t stride_h, int32_t stride_w, int32_t pad_h,
+                            int32_t pad_w, int32_t dil_h, int32_t dil_w, int64_t ho, int64_t wo, void *stream) {
+    if (!x || !out || n < 1 || h < 1 || w_ < 1 || c < 1 || ho < 1 || wo < 1 || r < 0 || s < 0) return IMCONV_EINVAL;
+    if (stride_h < 1 || stride_w < 1 || dil_h < 1 || dil_w < 1 || pad_h < 0 || pad_w < 0) return IMCONV_EINVAL;
+    return launch_gather(x, out, elem_bytes_, n, h, w_, c, 1, 1, r, s, stride_h, stride_w, pad_h, pad_w, dil_h, dil_w,
+                         ho, wo, 1, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int imconv_im2col_nhwc(const void *x, void *out, int32_t elem_bytes_, int64_t n, int64_t h, int64_t w_, int64_t c,
+                       int32_t hf, int32_t wf, int32_t stride_h, int32_t stride_w, int32_t pad_h, int32_t pad_w,
+                       int32_t dil_h, int32_t dil_w, int32_t channel_first, void *stream) {
+    if (!x || !out || n < 1 || h < 1 || w_ < 1 || c < 1 || hf < 1 || wf < 1) return IMCONV_EINVAL;
+    if (stride_h < 1 || stride_w < 1 || dil_h < 1 || dil_w < 1 || pad_h < 0 || pad_w < 0) return IMCONV_EINVAL;
+    const int64_t ho = imconv_out_extent(h, hf, stride_h, pad_h, dil_h);
+    const int64_t wo = imconv_out_extent(w_, wf, stride_w, pad_w, dil_w);
+    if (ho < 1 || wo < 1) return IMCONV_EINVAL;
+    return launch_gather(x, out, elem_bytes_, n, h, w_, c, hf, wf, -1, -1, stride_h, stride_w, pad_h, pad_w, dil_h,
+                         dil_w, ho, wo, channel_first ? 1 : 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int imconv_pad_copy(const void *src, void *dst, int32_t eb, int64_t outer, int64_t c, int64_t d, int64_t c_pad,
+                    int64_t d_pad, void *stream) {
+    if (!src || !dst || outer < 1 || c < 1 || d < 1 || c_pad < c || d_pad < d) return IMCONV_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const long long work = outer * c_pad * d_pad;
+#define IMCONV_PAD(T)                                                                                     \
+    pad_copy_kernel<T><<<grid_for(work), 256, 0, st>>>(reinterpret_cast<const T *>(src),                  \
+                                                       reinterpret_cast<T *>(dst), outer, static_cast<int>(c), \
+                                                       static_cast<int>(d), static_cast<int>(c_pad),           \
+                                                       static_cast<int>(d_pad))
+    switch (eb) {
+        case 1: IMCONV_PAD(uint8_t); break;
+        case 2: IMCONV_PAD(uint16_t); break;
+        case 4: IMCONV_PAD(uint32_t); break;
+        default: return IMCONV_EDTYPE;
+    }
+#undef IMCONV_PAD
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+}  // extern "C"

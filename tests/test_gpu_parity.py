@@ -1,0 +1,265 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the pinned oracle.
+
+Bars (BASELINE.json north_star):
+  * int8 -> int32: bit-exact;
+  * bf16 integer-valued data with fp32 output: bit-exact (values in [-4, 4]
+    are exact in bf16 and fp32 accumulation of the sums is exact);
+  * bf16 N(0,1) data: max|y - ref| / max|ref| <= 1e-2 against the fp32
+    oracle evaluated on the same bf16-rounded operands (REL_TOL below).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import conv_args, spec_from_vec
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-2        # north_star bf16 tolerance (normalised max error)
+REL_TOL_F32OUT = 1e-4  # fp32 output: only accumulation-order differences remain
+
+
+def _P():
+    import paper_2110_03901_b200 as P
+    return P
+
+
+def _norm_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def test_int_golden_bit_exact(golden):
+    P = _P()
+    for i in range(int(golden["n_int"])):
+        spec = spec_from_vec(golden[f"int{i}_spec"])
+        x = golden[f"int{i}_x"].astype(np.int64)
+        w = golden[f"int{i}_w"].astype(np.int64)
+        y = P._kernels.conv2d_nhwc(x, w, *conv_args(spec))
+        assert y.dtype == np.int64
+        assert np.array_equal(y, golden[f"int{i}_y"].astype(np.int64)), (i, spec)
+
+
+def test_int8_device_tensors_bit_exact(golden):
+    P = _P()
+    for i in range(int(golden["n_int"]) - 8, int(golden["n_int"])):
+        spec = spec_from_vec(golden[f"int{i}_spec"])
+        x = torch.from_numpy(golden[f"int{i}_x"]).cuda()
+        w = torch.from_numpy(golden[f"int{i}_w"]).cuda()
+        y = P._kernels.conv2d_nhwc(x, w, *conv_args(spec))
+        assert y.dtype == torch.int32 and y.is_cuda
+        assert np.array_equal(y.cpu().numpy(), golden[f"int{i}_y"]), i
+
+
+def test_bf16_integer_valued_exact(golden):
+    P = _P()
+    for i in range(0, int(golden["n_int"]) - 8):
+        spec = spec_from_vec(golden[f"int{i}_spec"])
+        x = torch.from_numpy(golden[f"int{i}_x"].astype(np.float32)).cuda().to(torch.bfloat16)
+        w = torch.from_numpy(golden[f"int{i}_w"].astype(np.float32)).cuda().to(torch.bfloat16)
+        y = P._kernels.conv2d_nhwc(x, w, *conv_args(spec), out_dtype=torch.float32)
+        assert np.array_equal(y.cpu().numpy(), golden[f"int{i}_y"].astype(np.float32)), (i, spec)
+
+
+def test_float_golden_tolerance(golden):
+    P = _P()
+    from oracle import oracle as O
+    for i in range(int(golden["n_flt"])):
+        spec = spec_from_vec(golden[f"flt{i}_spec"])
+        x, w = golden[f"flt{i}_x"], golden[f"flt{i}_w"]
+        # reference output on the exact inputs vs kernel on bf16-rounded inputs
+        y = P._kernels.conv2d_nhwc(x, w, *conv_args(spec))
+        assert y.dtype == np.float32
+        xb = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+        wb = torch.from_numpy(w).to(torch.bfloat16).float().numpy()
+        ref_b = O.conv2d_nhwc_taps(xb, wb, *conv_args(spec))
+        assert _norm_err(y, ref_b) <= REL_TOL_F32OUT, i
+        assert _norm_err(y, golden[f"flt{i}_y"]) <= 2 * REL_TOL, i
+
+
+@pytest.mark.parametrize("tile_n", [64, 128, 256])
+def test_block_shape_and_grid_invariance(rng, tile_n):
+    P = _P()
+    x = rng.integers(-4, 5, size=(3, 13, 11, 64)).astype(np.int64)
+    w = rng.integers(-4, 5, size=(3, 3, 64, 200)).astype(np.int64)
+    from oracle import oracle as O
+    want = O.conv2d_nhwc_i64(x, w, 1, 2, 1, 1, 2, 1)
+    xb = torch.from_numpy(x).float().cuda().bfloat16()
+    wb = torch.from_numpy(w).float().cuda().bfloat16()
+    for ctas in (0, 1, 5):
+        y = P._kernels.conv2d_nhwc(xb, wb, 1, 2, 1, 1, 2, 1, out_dtype=torch.float32, tile_n=tile_n, num_ctas=ctas)
+        assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), ctas
+
+
+@pytest.mark.parametrize("order", ["reuse_aware", "filter_major"])
+def test_subtile_orders_identical(rng, order):
+    P = _P()
+    x = rng.integers(-128, 128, size=(2, 20, 20, 256)).astype(np.int8)
+    w = rng.integers(-128, 128, size=(3, 3, 256, 128)).astype(np.int8)
+    from oracle import oracle as O
+    want = O.conv2d_nhwc_exact_f64(x, w, 2, 2, 1, 1, 1, 1)
+    y = P._kernels.conv2d_nhwc(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), 2, 2, 1, 1, 1, 1, order=order)
+    assert np.array_equal(y.cpu().numpy(), want)
+
+
+def test_small_channel_tap_packing(rng):
+    """C*elem < 128 B: several taps share one pipeline stage (16/32/64 B rows)."""
+    P = _P()
+    from oracle import oracle as O
+    for c in (3, 8, 16, 24, 32, 40):
+        x = rng.integers(-4, 5, size=(2, 15, 17, c)).astype(np.int64)
+        w = rng.integers(-4, 5, size=(7, 5, c, 24)).astype(np.int64)
+        want = O.conv2d_nhwc_i64(x, w, 2, 1, 3, 2, 1, 1)
+        xb = torch.from_numpy(x).float().cuda().bfloat16()
+        wb = torch.from_numpy(w).float().cuda().bfloat16()
+        y = P._kernels.conv2d_nhwc(xb, wb, 2, 1, 3, 2, 1, 1, out_dtype=torch.float32)
+        assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), c
+        yi = P._kernels.conv2d_nhwc(x, w, 2, 1, 3, 2, 1, 1)
+        assert np.array_equal(yi, want), c
+
+
+def test_gather_and_im2col_match_golden(golden):
+    P = _P()
+    for i in range(int(golden["n_gat"])):
+        spec = spec_from_vec(golden[f"gat{i}_spec"])
+        x = golden[f"gat{i}_x"]
+        r, s = (int(v) for v in golden[f"gat{i}_rs"])
+        g = P._kernels.tile_gather_nhwc(x, r, s, *conv_args(spec), spec.h_o, spec.w_o)
+        assert np.array_equal(g, golden[f"gat{i}_g"])
+        cf = P._kernels.im2col_nhwc(x, spec.h_f, spec.w_f, *conv_args(spec), True)
+        cl = P._kernels.im2col_nhwc(x, spec.h_f, spec.w_f, *conv_args(spec), False)
+        assert np.array_equal(cf, golden[f"gat{i}_cf"]), i
+        assert np.array_equal(cl, golden[f"gat{i}_cl"]), i
+
+
+def test_im2col_vector_path_bf16(rng):
+    P = _P()
+    from oracle import oracle as O
+    x = torch.randn(3, 14, 14, 64).bfloat16()
+    got = P._kernels.im2col_nhwc(x.cuda(), 3, 3, 2, 2, 1, 1, 1, 1, True).cpu()
+    want = O.im2col_nhwc(x.view(torch.int16).numpy(), 3, 3, 2, 2, 1, 1, 1, 1, True)
+    assert np.array_equal(got.view(torch.int16).numpy(), want)
+
+
+def test_explicit_path_equals_implicit(golden):
+    P = _P()
+    from paper_2110_03901_b200 import Layout, Method, Tensor
+    for i in range(int(golden["n_sim"])):
+        spec = spec_from_vec(golden[f"sim{i}_spec"])
+        x = Tensor.from_array(golden[f"sim{i}_x"].astype(np.int64), Layout.NHWC)
+        w = Tensor.from_array(golden[f"sim{i}_w"].astype(np.int64), Layout.HWCN)
+        for m in P.ALL_METHODS:
+            y = P.functional_ofmap(spec, m, x, w)
+            assert np.array_equal(y.view(), golden[f"sim{i}_y"].astype(np.int64)), (i, m)
+
+
+def test_gemm_matches_oracle(rng):
+    P = _P()
+    from paper_2110_03901_b200 import Layout, Tensor
+    a = rng.integers(-6, 7, size=(300, 96)).astype(np.int64)
+    b = rng.integers(-6, 7, size=(96, 40)).astype(np.int64)
+    got = P.gemm(Tensor.from_array(a, Layout.ROW_MAJOR), Tensor.from_array(b, Layout.ROW_MAJOR))
+    assert np.array_equal(got.view(), a @ b)
+
+
+def test_direct_conv_api_and_shape_errors(rng):
+    P = _P()
+    from paper_2110_03901_b200 import ConvSpec, Layout, ShapeError, Tensor
+    spec = ConvSpec.square(1, 1, 1, 1, 1)
+    out = P.direct_conv(Tensor.from_array(np.array([[[[3.0]]]]), Layout.NHWC),
+                        Tensor.from_array(np.array([[[[2.0]]]]), Layout.HWCN), spec)
+    assert out.data.tolist() == [6.0]
+    spec = ConvSpec.square(1, 1, 3, 1, 3)
+    out = P.direct_conv(Tensor.from_array(np.ones((1, 3, 3, 1)), Layout.NHWC),
+                        Tensor.from_array(np.ones((3, 3, 1, 1)), Layout.HWCN), spec)
+    assert out.dims == (1, 1, 1, 1) and out.data.tolist() == [9.0]
+    with pytest.raises(ShapeError):
+        P.direct_conv(Tensor.from_array(np.zeros((1, 4, 4, 3)), Layout.NHWC),
+                      Tensor.from_array(np.zeros((1, 1, 2, 1)), Layout.HWCN), ConvSpec.square(1, 2, 4, 1, 1))
+    with pytest.raises(ValueError):
+        P._kernels.conv2d_nhwc(np.full((1, 4, 4, 16), 300), np.ones((1, 1, 16, 8), np.int64), 1, 1, 0, 0, 1, 1)
+    with pytest.raises(ValueError):
+        P._kernels.conv2d_nhwc(np.ones((1, 4, 4, 3)), np.ones((1, 1, 2, 8)), 1, 1, 0, 0, 1, 1)
+
+
+def test_nchw_input_relayout(rng):
+    P = _P()
+    from paper_2110_03901_b200 import ConvSpec, Layout, Tensor
+    from oracle import oracle as O
+    spec = ConvSpec.square(2, 8, 9, 16, 3, stride=2, pad=1)
+    x = rng.integers(-4, 5, size=(2, 9, 9, 8)).astype(np.int64)
+    w = rng.integers(-4, 5, size=(3, 3, 8, 16)).astype(np.int64)
+    got = P.direct_conv(Tensor.from_array(x.transpose(0, 3, 1, 2), Layout.NCHW),
+                        Tensor.from_array(w, Layout.HWCN), spec)
+    assert np.array_equal(got.view(), O.conv2d_nhwc_i64(x, w, 2, 2, 1, 1, 1, 1))
+
+
+def test_evaluate_plan_orders(rng):
+    P = _P()
+    from paper_2110_03901_b200 import ConvSpec, Layout, Tensor
+    from paper_2110_03901_b200.blocksched import SubtileOrder, evaluate_plan, order_subtiles, partition
+    from oracle import oracle as O
+    spec = ConvSpec.square(2, 3, 8, 4, 3, stride=2, pad=1)
+    x = rng.integers(-4, 5, size=(2, 8, 8, 3)).astype(np.int64)
+    w = rng.integers(-4, 5, size=(3, 3, 3, 4)).astype(np.int64)
+    want = O.conv2d_nhwc_i64(x, w, 2, 2, 1, 1, 1, 1)
+    plan = partition(spec, 5, 3, 2)
+    fm = order_subtiles(plan, SubtileOrder.FILTER_MAJOR)
+    ra = order_subtiles(plan, SubtileOrder.REUSE_AWARE)
+    sh = list(fm)
+    rng.shuffle(sh)
+    for order in (fm, ra, sh):
+        out = evaluate_plan(plan, order, Tensor.from_array(x, Layout.NHWC), Tensor.from_array(w, Layout.HWCN))
+        assert np.array_equal(out.view(), want)
+    with pytest.raises(ValueError):
+        evaluate_plan(plan, fm[:-1], Tensor.from_array(x, Layout.NHWC), Tensor.from_array(w, Layout.HWCN))
+
+
+# ------------------------------------------------------------------ BASELINE configs
+
+def _layer_check(layer, n=None, seed=0):
+    P = _P()
+    from oracle import oracle as O
+    sp = layer.spec if n is None else layer.spec.with_batch(n)
+    x, w = P.workloads.synthetic_operands(layer, seed=seed, n=n)
+    xd, wd = x.cuda(), w.cuda()
+    if layer.dtype == "int8":
+        y = P._kernels.conv2d_nhwc(xd, wd, *conv_args(sp))
+        want = O.conv2d_nhwc_exact_f64(x.numpy(), w.numpy(), *conv_args(sp))
+        assert np.array_equal(y.cpu().numpy().astype(np.int64), want), layer.name
+        return 0.0
+    y = P._kernels.conv2d_nhwc(xd, wd, *conv_args(sp))  # bf16 out
+    assert y.dtype == torch.bfloat16
+    ref = O.conv2d_nhwc_taps(x.float().numpy(), w.float().numpy(), *conv_args(sp))
+    err = _norm_err(y.float().cpu().numpy(), ref)
+    assert err <= REL_TOL, (layer.name, err)
+    y32 = P._kernels.conv2d_nhwc(xd, wd, *conv_args(sp), out_dtype=torch.float32)
+    err32 = _norm_err(y32.cpu().numpy(), ref)
+    assert err32 <= REL_TOL_F32OUT, (layer.name, err32)
+    return err
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3"])
+def test_baseline_config_full_size(cfg):
+    P = _P()
+    for layer in P.workloads.baseline_configs()[cfg]:
+        _layer_check(layer)
+
+
+def test_baseline_cfg5_int8_full_size_bit_exact():
+    P = _P()
+    for layer in P.workloads.baseline_configs()["cfg5"]:
+        _layer_check(layer)
+
+
+def test_resnet50_layers_reduced_batch():
+    P = _P()
+    seen = set()
+    for layer in P.workloads.resnet50_layers(2):
+        key = layer.spec
+        if key in seen:
+            continue
+        seen.add(key)
+        _layer_check(layer)
