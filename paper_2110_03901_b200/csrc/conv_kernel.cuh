@@ -31,6 +31,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <type_traits>
 
 #include "ptx.cuh"
 
@@ -97,50 +98,41 @@ __device__ __forceinline__ uint32_t make_idesc() {
 }
 
 template <int OUT>
-__device__ __forceinline__ void store_row_chunk(const ConvParams &p, long long m, int col0, const uint32_t (&v)[32]) {
+struct OutTraits {
+    static constexpr int kBytes = (OUT == OUT_BF16 || OUT == OUT_F16) ? 2 : 4;
+    static constexpr int kRowBytes = 32 * kBytes;  // one 32-column epilogue chunk of one output row
+};
+
+// Convert one row's 32 accumulator words and write them into the warp's
+// staging tile (32 rows x kRowBytes) in the TMA swizzle layout: SW64 for
+// 16-bit outputs (Swizzle<2,4,3>), SW128 for 32-bit outputs (Swizzle<3,4,3>).
+template <int OUT>
+__device__ __forceinline__ void stage_row_chunk(uint8_t *buf, uint32_t row, const uint32_t (&v)[32]) {
+    constexpr int RB = OutTraits<OUT>::kRowBytes;
+    uint8_t *dst = buf + row * RB;
     if constexpr (OUT == OUT_BF16 || OUT == OUT_F16) {
-        using T = typename std::conditional<OUT == OUT_BF16, __nv_bfloat16, __half>::type;
-        T *row = reinterpret_cast<T *>(p.y) + m * p.ldy;
-        if (col0 + 32 <= p.k && (p.k & 7) == 0) {
-            uint32_t packed[16];
+        uint32_t packed[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
-                if constexpr (OUT == OUT_BF16) {
-                    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
-                    packed[i] = *reinterpret_cast<uint32_t *>(&t);
-                } else {
-                    __half2 t = __floats2half2_rn(a, b);
-                    packed[i] = *reinterpret_cast<uint32_t *>(&t);
-                }
-            }
-            uint4 *dst = reinterpret_cast<uint4 *>(row + col0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                if (col0 + i < p.k) {
-                    if constexpr (OUT == OUT_BF16)
-                        row[col0 + i] = __float2bfloat16_rn(__uint_as_float(v[i]));
-                    else
-                        row[col0 + i] = __float2half_rn(__uint_as_float(v[i]));
-                }
+        for (int i = 0; i < 16; ++i) {
+            const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
+            if constexpr (OUT == OUT_BF16) {
+                __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+                packed[i] = *reinterpret_cast<uint32_t *>(&t);
+            } else {
+                __half2 t = __floats2half2_rn(a, b);
+                packed[i] = *reinterpret_cast<uint32_t *>(&t);
             }
         }
+        const uint32_t swz = (row >> 1) & 3;
+#pragma unroll
+        for (uint32_t c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4 *>(dst + ((c ^ swz) << 4)) =
+                make_uint4(packed[4 * c], packed[4 * c + 1], packed[4 * c + 2], packed[4 * c + 3]);
     } else {
-        // fp32 or int32: raw 32-bit accumulator words
-        uint32_t *row = reinterpret_cast<uint32_t *>(p.y) + m * p.ldy;
-        if (col0 + 32 <= p.k && (p.k & 3) == 0) {
-            uint4 *dst = reinterpret_cast<uint4 *>(row + col0);
+        const uint32_t swz = row & 7;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (col0 + i < p.k) row[col0 + i] = v[i];
-        }
+        for (uint32_t c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4 *>(dst + ((c ^ swz) << 4)) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
 }
 
@@ -153,7 +145,8 @@ struct ConvCfg {
     static constexpr int kMmaK = 32 / kE;            // reduction elements per tcgen05.mma
     static constexpr int kMmaPerStage = kBKE / kMmaK;  // = 4
     static constexpr int kTmemCols = 2 * BN;         // double-buffered accumulator
-    static constexpr int kSmemBytes = STAGES * (kAStage + kBStage) + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kStageOut = 2 * 32 * OutTraits<OUT>::kRowBytes;  // per epilogue warp: 2 buffers
+    static constexpr int kSmemBytes = STAGES * (kAStage + kBStage) + 4 * kStageOut + 1024 /*align*/ + 256 /*barriers*/;
     static_assert(BN % kNC == 0, "BN must be a multiple of the swizzle atom width");
     static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
 };
@@ -161,13 +154,14 @@ struct ConvCfg {
 template <int ELEM, int OUT, int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    const ConvParams p) {
+                    const __grid_constant__ CUtensorMap tmap_y, const ConvParams p) {
     using Cfg = ConvCfg<ELEM, OUT, BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *smem_a = smem;
     uint8_t *smem_b = smem + STAGES * kAStage;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_b + STAGES * Cfg::kBStage);
+    uint8_t *smem_out = smem_b + STAGES * Cfg::kBStage;  // epilogue staging, 1024-aligned
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_out + 4 * Cfg::kStageOut);
     uint64_t *full = bars;
     uint64_t *empty = bars + STAGES;
     uint64_t *tfull = bars + 2 * STAGES;
@@ -181,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
         ptx::prefetch_tmap(&tmap_b);
+        ptx::prefetch_tmap(&tmap_y);
         for (int i = 0; i < STAGES; ++i) {
             ptx::mbar_init(&full[i], 1);
             ptx::mbar_init(&empty[i], 1);
@@ -319,25 +314,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (acc == 0) acc_phase ^= 1;
         }
     } else if (warp >= 4) {
-        // ===================== epilogue: TMEM -> registers -> NHWC =====================
-        const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+        // ============ epilogue: TMEM -> registers -> swizzled smem -> TMA store ============
+        const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32) = block rows
+        uint8_t *stage_buf = smem_out + quarter * Cfg::kStageOut;
+        constexpr int kBuf = 32 * OutTraits<OUT>::kRowBytes;
         int acc = 0;
         uint32_t acc_phase = 0;
+        uint32_t chunk_ctr = 0;
         for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
-            const long long m = m_tile * kBM + quarter * 32 + lane;
+            const int row0 = static_cast<int>(m_tile * kBM) + quarter * 32;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int j = 0; j < BN / 32; ++j) {
+                const int col0 = n_tile * BN + j * 32;
                 uint32_t v[32];
                 const uint32_t taddr =
                     tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + j * 32);
                 ptx::tmem_ld_32x32b_x32(taddr, v);
                 ptx::tmem_ld_wait();
-                const int col0 = n_tile * BN + j * 32;
-                if (m < p.m && col0 < p.k) store_row_chunk<OUT>(p, m, col0, v);
+                if (col0 >= p.k) continue;  // warp-uniform: whole chunk past the last channel
+                uint8_t *buf = stage_buf + (chunk_ctr & 1) * kBuf;
+                if (lane == 0) ptx::tma_store_wait_read<1>();  // the store issued 2 chunks ago has read buf
+                __syncwarp();
+                stage_row_chunk<OUT>(buf, lane, v);
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tmap_y, buf, col0, row0);  // rows >= M / cols >= K are clipped
+                    ptx::tma_store_commit();
+                }
+                ++chunk_ctr;
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -345,6 +354,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        if (lane == 0) ptx::tma_store_wait<0>();
+        __syncwarp();
     }
 
     __syncthreads();

@@ -80,7 +80,8 @@ CUtensorMapDataType tmap_dtype(int in_dtype) {
 int elem_bytes(int in_dtype) { return in_dtype == IMCONV_I8 ? 1 : 2; }
 
 template <int ELEM, int OUT, int BN, int STAGES>
-int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvParams &p, int grid, cudaStream_t st) {
+int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const ConvParams &p, int grid,
+                cudaStream_t st) {
     using Cfg = ConvCfg<ELEM, OUT, BN, STAGES>;
     auto kern = conv_fwd_kernel<ELEM, OUT, BN, STAGES>;
     static std::once_flag once;
@@ -89,7 +90,7 @@ int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvParams &
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(ta, tb, p);
+    kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(ta, tb, ty, p);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
@@ -97,15 +98,15 @@ int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const ConvParams &
 
 // BN -> pipeline depth that fits ~200 KB of shared memory.
 template <int ELEM, int OUT>
-int dispatch_bn(int bn, const CUtensorMap &ta, const CUtensorMap &tb, const ConvParams &p, int grid,
-                cudaStream_t st) {
+int dispatch_bn(int bn, const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const ConvParams &p,
+                int grid, cudaStream_t st) {
     if constexpr (ELEM == ELEM_I8) {
-        if (bn == 128) return launch_conv<ELEM, OUT, 128, 6>(ta, tb, p, grid, st);
-        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4>(ta, tb, p, grid, st);
+        if (bn == 128) return launch_conv<ELEM, OUT, 128, 6>(ta, tb, ty, p, grid, st);
+        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4>(ta, tb, ty, p, grid, st);
     } else {
-        if (bn == 64) return launch_conv<ELEM, OUT, 64, 8>(ta, tb, p, grid, st);
-        if (bn == 128) return launch_conv<ELEM, OUT, 128, 6>(ta, tb, p, grid, st);
-        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4>(ta, tb, p, grid, st);
+        if (bn == 64) return launch_conv<ELEM, OUT, 64, 8>(ta, tb, ty, p, grid, st);
+        if (bn == 128) return launch_conv<ELEM, OUT, 128, 6>(ta, tb, ty, p, grid, st);
+        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4>(ta, tb, ty, p, grid, st);
     }
     return IMCONV_EINVAL;
 }
@@ -193,7 +194,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         return IMCONV_ERANGE;
     if (a->stride_h > 8 || a->stride_w > 8) return IMCONV_ERANGE;
     const int64_t M = N * P * Q;
-    if (M >= (1ll << 40) || R * S * C >= (1ll << 31) || H * W >= (1ll << 31)) return IMCONV_ERANGE;
+    if (M >= (1ll << 31) || R * S * C >= (1ll << 31) || H * W >= (1ll << 31)) return IMCONV_ERANGE;
 
     int rc = load_driver_entry_points();
     if (rc) return rc;
@@ -252,6 +253,25 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
     }
 
+    // ---- output: tiled map over y viewed as (M, K), 32x32 store boxes ----
+    CUtensorMap ty;
+    std::memset(&ty, 0, sizeof(ty));
+    {
+        const int eo = (a->out_dtype == IMCONV_F32 || a->out_dtype == IMCONV_I32) ? 4 : 2;
+        CUtensorMapDataType dt = a->out_dtype == IMCONV_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : a->out_dtype == IMCONV_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                 : a->out_dtype == IMCONV_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
+        cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * eo)};
+        cuuint32_t box[2] = {32, 32};
+        cuuint32_t estride[2] = {1, 1};
+        CUresult cr = g_encode_tiled(&ty, dt, 2, a->y, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     eo == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
+    }
+
     ConvParams p{};
     p.n = static_cast<int>(N);
     p.h = static_cast<int>(H);
@@ -287,12 +307,12 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
 
     switch (a->in_dtype) {
         case IMCONV_BF16:
-            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, ta, tb, p, grid, st)
-                                              : dispatch_bn<ELEM_BF16, OUT_BF16>(bn, ta, tb, p, grid, st);
+            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, grid, st)
+                                              : dispatch_bn<ELEM_BF16, OUT_BF16>(bn, ta, tb, ty, p, grid, st);
         case IMCONV_F16:
-            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_F16, OUT_F32>(bn, ta, tb, p, grid, st)
-                                              : dispatch_bn<ELEM_F16, OUT_F16>(bn, ta, tb, p, grid, st);
-        case IMCONV_I8: return dispatch_bn<ELEM_I8, OUT_I32>(bn, ta, tb, p, grid, st);
+            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_F16, OUT_F32>(bn, ta, tb, ty, p, grid, st)
+                                              : dispatch_bn<ELEM_F16, OUT_F16>(bn, ta, tb, ty, p, grid, st);
+        case IMCONV_I8: return dispatch_bn<ELEM_I8, OUT_I32>(bn, ta, tb, ty, p, grid, st);
         default: return IMCONV_EDTYPE;
     }
 }
