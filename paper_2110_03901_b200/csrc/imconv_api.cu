@@ -18,6 +18,7 @@
 #include "../../include/imconv.h"
 #include "aux_kernels.cuh"
 #include "conv_kernel.cuh"
+#include "conv_rowband.cuh"
 
 namespace imconv {
 namespace {
@@ -122,6 +123,155 @@ int pick_bn(int in_dtype, int64_t k, int requested) {
     return static_cast<int>(bn);
 }
 
+constexpr int kMaxDynSmem = 227 * 1024;
+
+inline int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+
+template <int ELEM, int OUT, int BN, int TP>
+int launch_rowband(const CUtensorMap &tx, const CUtensorMap &tw, const CUtensorMap &ty, const RowbandParams &p,
+                   int smem, int grid, cudaStream_t st) {
+    auto kern = conv_rowband_kernel<ELEM, OUT, BN, TP>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    });
+    if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
+    kern<<<grid, kThreads, smem, st>>>(tx, tw, ty, p);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+// Row-band path for 16-byte pixels (bf16/fp16, C = 8).  Returns 1 when the
+// layer does not qualify (the caller then uses the generic kernel).
+int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st) {
+    if (!(a->in_dtype == IMCONV_BF16 || a->in_dtype == IMCONV_F16) || a->c != 8) return 1;
+    if (a->tile_n != 0 || a->k > 256 || a->s > 2 * kMaxPairs || a->stride_w > 8) return 1;
+    const int K = static_cast<int>(a->k), R = static_cast<int>(a->r), S = static_cast<int>(a->s);
+    const int BN = K <= 64 ? 64 : (K <= 128 ? 128 : 256);
+    const int TP = 256 / BN;
+    RowbandParams p{};
+    p.n = static_cast<int>(a->n);
+    p.h = static_cast<int>(a->h);
+    p.w = static_cast<int>(a->w_);
+    p.k = K;
+    p.r = R;
+    p.s = S;
+    p.sh = a->stride_h;
+    p.sw = a->stride_w;
+    p.ph = a->pad_h;
+    p.pw = a->pad_w;
+    p.dh = a->dil_h;
+    p.dw = a->dil_w;
+    p.p = static_cast<int>(P);
+    p.q = static_cast<int>(Q);
+    p.p_groups = static_cast<int>((P + TP - 1) / TP);
+    p.q_blocks = static_cast<int>((Q + 127) / 128);
+    p.tiles = static_cast<long long>(p.n) * p.p_groups * p.q_blocks;
+    int t_s[2 * kMaxPairs], e_s[2 * kMaxPairs];
+    int t_min = 1 << 30, t_max = -(1 << 30);
+    for (int s = 0; s < S; ++s) {
+        const int off = s * p.dw - p.pw;
+        t_s[s] = floordiv(off, p.sw);
+        e_s[s] = off - p.sw * t_s[s];
+        t_min = std::min(t_min, t_s[s]);
+        t_max = std::max(t_max, t_s[s]);
+    }
+    p.t_min = t_min;
+    p.box_pix = ((256 / p.sw) / 8) * 8;
+    const int needed = static_cast<int>(std::min<int64_t>(Q, 128)) + t_max - t_min;
+    p.n_boxes = (needed + p.box_pix - 1) / p.box_pix;
+    const int plane_pix = std::max(128 + t_max - t_min, p.n_boxes * p.box_pix);
+    p.plane_bytes = ((plane_pix * 16 + 127) / 128) * 128;
+    p.a_stage_bytes = p.sw * p.plane_bytes;
+    p.in_rows = (TP - 1) * p.sh + (R - 1) * p.dh + 1;
+    p.npairs = (S + 1) / 2;
+    p.b_chunk_bytes = R * p.npairs * 2 * 1024;
+    p.b_bytes = (BN / 64) * p.b_chunk_bytes;
+    // taps ordered by their run address inside a stage, paired neighbour-wise
+    int order[2 * kMaxPairs], addr[2 * kMaxPairs];
+    for (int s = 0; s < S; ++s) {
+        order[s] = s;
+        addr[s] = e_s[s] * p.plane_bytes + (t_s[s] - t_min) * 16;
+    }
+    std::sort(order, order + S, [&](int x, int y) { return addr[x] < addr[y]; });
+    for (int pr = 0; pr < p.npairs; ++pr) {
+        const int s0 = order[2 * pr];
+        const int s1 = 2 * pr + 1 < S ? order[2 * pr + 1] : -1;
+        p.pair_s0[pr] = s0;
+        p.pair_s1[pr] = s1;
+        p.pair_a_off[pr] = addr[s0];
+        p.pair_lbo[pr] = s1 >= 0 ? addr[s1] - addr[s0] : 16;  // zero tap: any finite run
+    }
+    const int kStageOut = 2 * 32 * ((a->out_dtype == IMCONV_F32) ? 128 : 64);
+    const int fixed = p.b_bytes + 4 * kStageOut + 1024 + 512;
+    const int room = kMaxDynSmem - fixed;
+    p.n_stages = std::min(24, room / p.a_stage_bytes);
+    if (p.b_bytes > 128 * 1024 || p.n_stages < 3) return 1;
+    const int smem = fixed + p.n_stages * p.a_stage_bytes;
+
+    // plane map: tiled 4-D over NHWC with element stride sw along W
+    CUtensorMap tx, tw, ty;
+    std::memset(&tx, 0, sizeof(tx));
+    std::memset(&tw, 0, sizeof(tw));
+    std::memset(&ty, 0, sizeof(ty));
+    const int64_t N = a->n, H = a->h, W = a->w_, C = 8;
+    {
+        cuuint64_t gdim[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(N)};
+        cuuint64_t gstride[3] = {static_cast<cuuint64_t>(C * 2), static_cast<cuuint64_t>(W * C * 2),
+                                 static_cast<cuuint64_t>(H * W * C * 2)};
+        cuuint32_t box[4] = {8, static_cast<cuuint32_t>(p.box_pix * p.sw), 1, 1};
+        cuuint32_t es[4] = {1, static_cast<cuuint32_t>(p.sw), 1, 1};
+        if (g_encode_tiled(&tx, tmap_dtype(a->in_dtype), 4, const_cast<void *>(a->x), gdim, gstride, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    {
+        cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(R * S * C)};
+        cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * 2)};
+        cuuint32_t box[2] = {64, 8};
+        cuuint32_t es[2] = {1, 1};
+        if (g_encode_tiled(&tw, tmap_dtype(a->in_dtype), 2, const_cast<void *>(a->w), gdim, gstride, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    {
+        const int eo = a->out_dtype == IMCONV_F32 ? 4 : 2;
+        CUtensorMapDataType dt = a->out_dtype == IMCONV_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : a->out_dtype == IMCONV_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        cuuint64_t gdim[4] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(P),
+                              static_cast<cuuint64_t>(N)};
+        cuuint64_t gstride[3] = {static_cast<cuuint64_t>(K * eo), static_cast<cuuint64_t>(Q * K * eo),
+                                 static_cast<cuuint64_t>(P * Q * K * eo)};
+        cuuint32_t box[4] = {32, 32, 1, 1};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (g_encode_tiled(&ty, dt, 4, a->y, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           eo == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    int grid = a->num_ctas > 0 ? a->num_ctas : sms;
+    if (grid > p.tiles) grid = static_cast<int>(p.tiles);
+    const bool f32 = a->out_dtype == IMCONV_F32;
+#define IMCONV_RB(EL, OUTK)                                                                          \
+    switch (BN) {                                                                                    \
+        case 64: return launch_rowband<EL, OUTK, 64, 4>(tx, tw, ty, p, smem, grid, st);              \
+        case 128: return launch_rowband<EL, OUTK, 128, 2>(tx, tw, ty, p, smem, grid, st);            \
+        default: return launch_rowband<EL, OUTK, 256, 1>(tx, tw, ty, p, smem, grid, st);             \
+    }
+    if (a->in_dtype == IMCONV_BF16) {
+        if (f32) { IMCONV_RB(ELEM_BF16, OUT_F32) } else { IMCONV_RB(ELEM_BF16, OUT_BF16) }
+    } else {
+        if (f32) { IMCONV_RB(ELEM_F16, OUT_F32) } else { IMCONV_RB(ELEM_F16, OUT_F16) }
+    }
+#undef IMCONV_RB
+}
+
 }  // namespace
 }  // namespace imconv
 
@@ -201,6 +351,11 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     int sms = 0;
     rc = sm_count_for_current_device(&sms);
     if (rc) return rc;
+
+    if (a->order != IMCONV_ORDER_FILTER_MAJOR) {
+        const int rb = try_rowband(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
+        if (rb != 1) return rb;
+    }
 
     const int bn = pick_bn(a->in_dtype, K, a->tile_n);
     if (bn < 0) return IMCONV_EINVAL;

@@ -1,0 +1,58 @@
+#!/usr/bin/env python
+"""Run one BASELINE layer a few times on cuda:0 (for ncu / quick timing).
+
+  python tools/run_layer.py --layer stem [--n 256] [--reps 5] [--tile-n 0] [--order reuse_aware]
+"""
+
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layer", default="stem")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--tile-n", type=int, default=0)
+    ap.add_argument("--order", default="reuse_aware")
+    ap.add_argument("--explicit", action="store_true", help="K3 im2col + K4 GEMM instead of the implicit kernel")
+    args = ap.parse_args()
+
+    import torch
+    from paper_2110_03901_b200 import _lib
+    from paper_2110_03901_b200._kernels import conv_device, gemm_device
+    from paper_2110_03901_b200.workloads import baseline_configs
+    import paper_2110_03901_b200._kernels as K
+
+    layers = {l.name: l for cfg in baseline_configs().values() for l in cfg}
+    layer = layers[args.layer]
+    sp = layer.spec if args.n is None else layer.spec.with_batch(args.n)
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    if layer.dtype == "int8":
+        x = torch.randint(-128, 128, (sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev, dtype=torch.int16).to(torch.int8)
+        w = torch.randint(-128, 128, (sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev, dtype=torch.int16).to(torch.int8)
+    else:
+        x = torch.randn((sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev).to(torch.bfloat16)
+        w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev) * 0.05).to(torch.bfloat16)
+    order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[args.order]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for i in range(args.reps + 1):
+        if i == 1:
+            ev[0].record()
+        if args.explicit:
+            low = K.im2col_nhwc(x, sp.h_f, sp.w_f, *sp.conv_args(), True)
+            gemm_device(low, w.reshape(-1, sp.c_o))
+        else:
+            conv_device(x, w, *sp.conv_args(), tile_n=args.tile_n, order=order)
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / args.reps
+    print(f"{args.layer} n={sp.n}: {ms:.4f} ms  {sp.flops / ms / 1e9:.1f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    main()
