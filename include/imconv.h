@@ -156,6 +156,14 @@ IMCONV_API const char *imconv_strerror(int code);
 IMCONV_API int64_t imconv_launch_count(void);
 IMCONV_API void imconv_reset_launch_count(void);
 
+/* Instrumentation: when set (device buffer of >= 8 * num_ctas int64), the
+ * next launches record per-CTA role cycles and blocking-wait cycles into it.
+ * NULL (the default) disables recording. */
+IMCONV_API void imconv_debug_set_buffer(void *dev_buf);
+/* Instrumentation only: bit flags that switch off pipeline roles of the
+ * specialised kernels (results are then WRONG); 0 = normal operation. */
+IMCONV_API void imconv_debug_set_flags(int flags);
+
 #ifdef __cplusplus
 }
 #endif

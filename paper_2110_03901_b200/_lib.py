@@ -21,6 +21,7 @@ EXPORTED = (
     "imconv_conv2d_nhwc", "imconv_out_extent", "imconv_gemm", "imconv_tile_gather_nhwc",
     "imconv_im2col_nhwc", "imconv_pad_copy", "imconv_lru_simulate", "imconv_abi_version",
     "imconv_device_sm_count", "imconv_strerror", "imconv_launch_count", "imconv_reset_launch_count",
+    "imconv_debug_set_buffer", "imconv_debug_set_flags",
 )
 
 
@@ -77,6 +78,10 @@ def _load():
     L.imconv_launch_count.restype = i64
     L.imconv_reset_launch_count.argtypes = []
     L.imconv_reset_launch_count.restype = None
+    L.imconv_debug_set_buffer.argtypes = [vp]
+    L.imconv_debug_set_buffer.restype = None
+    L.imconv_debug_set_flags.argtypes = [ctypes.c_int]
+    L.imconv_debug_set_flags.restype = None
     return L
 
 

@@ -62,7 +62,14 @@ struct ConvParams {
     int order;           // 0 reuse-aware, 1 filter-major
     void *y;
     long long ldy;       // = k
+    long long *dbg;      // optional per-CTA role / wait-cycle counters (instrumentation), else nullptr
 };
+
+__device__ __forceinline__ void timed_wait_g(uint64_t *bar, uint32_t parity, long long &acc) {
+    const long long t0 = clock64();
+    ptx::mbar_wait(bar, parity);
+    acc += clock64() - t0;
+}
 
 template <int ELEM>
 struct ElemTraits;
@@ -200,6 +207,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int pq = p.p * p.q;
             int stage = 0;
             uint32_t phase = 0;
+            long long w_empty = 0;
+            const long long t_start = clock64();
             for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
                 const long long m_tile = tile / p.n_tiles;
                 const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int h0 = p0 * p.sh - p.ph;
                 const int nb0 = n_tile * BN;
                 for (int kb = 0; kb < p.k_stages; ++kb) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    timed_wait_g(&empty[stage], phase ^ 1, w_empty);
                     ptx::mbar_arrive_expect_tx(&full[stage], kAStage + Cfg::kBStage);
                     uint8_t *a_dst = smem_a + stage * kAStage;
                     uint8_t *b_dst = smem_b + stage * Cfg::kBStage;
@@ -256,6 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            if (p.dbg) {
+                p.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
+                p.dbg[blockIdx.x * 8 + 1] = w_empty;
+            }
         }
         __syncwarp();
     } else if (warp == 1) {
@@ -268,50 +281,65 @@ __global__ void __launch_bounds__(kThreads, 1)
             case A_SW32: a_lbo = 16; a_sbo = 256; a_layout = ptx::LAYOUT_SW32; break;
             default: a_lbo = kBM * 16; a_sbo = 128; a_layout = ptx::LAYOUT_NONE; break;
         }
+        // descriptors built once; per MMA only the 14-bit start-address field
+        // moves (stage and k-step offsets >> 4 are added to the low word)
+        uint32_t a_kk[Cfg::kMmaPerStage];
+#pragma unroll
+        for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk) {
+            uint32_t off;
+            switch (p.a_layout) {
+                case A_SW128: off = kk * 32; break;
+                case A_SW64: off = (kk >> 1) * (kBM * 64) + (kk & 1) * 32; break;
+                case A_SW32: off = kk * (kBM * 32); break;
+                default: off = kk * 2 * (kBM * 16); break;
+            }
+            a_kk[kk] = off >> 4;
+        }
+        const uint64_t adesc0 = ptx::smem_desc(ptx::smem_u32(smem_a), a_lbo, a_sbo, a_layout);
+        const uint64_t bdesc0 =
+            ptx::smem_desc(ptx::smem_u32(smem_b), Cfg::kBKE * kRowBytes, 1024, ptx::LAYOUT_SW128);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
+        long long w_tempty = 0, w_full = 0;
+        const long long t_start = clock64();
         for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+            timed_wait_g(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
             for (int kb = 0; kb < p.k_stages; ++kb) {
-                ptx::mbar_wait(&full[stage], phase);
+                timed_wait_g(&full[stage], phase, w_full);
                 ptx::tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a_base = ptx::smem_u32(smem_a + stage * kAStage);
-                    const uint32_t b_base = ptx::smem_u32(smem_b + stage * Cfg::kBStage);
+                {
+                    // warp-collective issue: uniform descriptors, elect.sync inside the asm
+                    const uint64_t a_st = adesc0 + static_cast<uint64_t>((stage * kAStage) >> 4);
+                    const uint64_t b_st = bdesc0 + static_cast<uint64_t>((stage * Cfg::kBStage) >> 4);
 #pragma unroll
                     for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk) {
-                        uint32_t a_off;
-                        switch (p.a_layout) {
-                            case A_SW128: a_off = kk * 32; break;
-                            case A_SW64: a_off = (kk >> 1) * (kBM * 64) + (kk & 1) * 32; break;
-                            case A_SW32: a_off = kk * (kBM * 32); break;
-                            default: a_off = kk * 2 * (kBM * 16); break;
-                        }
-                        const uint64_t adesc = ptx::smem_desc(a_base + a_off, a_lbo, a_sbo, a_layout);
-                        const uint64_t bdesc = ptx::smem_desc(b_base + kk * (Cfg::kMmaK * kRowBytes),
-                                                              Cfg::kBKE * kRowBytes, 1024, ptx::LAYOUT_SW128);
+                        const uint64_t adesc = a_st + a_kk[kk];
+                        const uint64_t bdesc = b_st + static_cast<uint64_t>((kk * Cfg::kMmaK * kRowBytes) >> 4);
                         const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
                         if constexpr (ELEM == ELEM_I8)
-                            ptx::mma_i8(d_tmem, adesc, bdesc, idesc, accum);
+                            ptx::mma_i8_elect(d_tmem, adesc, bdesc, idesc, accum);
                         else
-                            ptx::mma_f16(d_tmem, adesc, bdesc, idesc, accum);
+                            ptx::mma_f16_elect(d_tmem, adesc, bdesc, idesc, accum);
                     }
-                    ptx::mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+                    ptx::mma_commit_elect(&empty[stage]);  // frees the smem slot once these MMAs retire
                 }
-                __syncwarp();
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (lane == 0) ptx::mma_commit(&tfull[acc]);  // accumulator complete -> epilogue
-            __syncwarp();
+            ptx::mma_commit_elect(&tfull[acc]);  // accumulator complete -> epilogue
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
+        }
+        if (p.dbg && lane == 0) {
+            p.dbg[blockIdx.x * 8 + 2] = clock64() - t_start;
+            p.dbg[blockIdx.x * 8 + 3] = w_tempty;
+            p.dbg[blockIdx.x * 8 + 4] = w_full;
         }
     } else if (warp >= 4) {
         // ============ epilogue: TMEM -> registers -> swizzled smem -> TMA store ============
@@ -321,11 +349,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         uint32_t chunk_ctr = 0;
+        long long w_tfull = 0;
+        const long long t_start = clock64();
         for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
             const int row0 = static_cast<int>(m_tile * kBM) + quarter * 32;
-            ptx::mbar_wait(&tfull[acc], acc_phase);
+            timed_wait_g(&tfull[acc], acc_phase, w_tfull);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int j = 0; j < BN / 32; ++j) {
@@ -356,6 +386,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (lane == 0) ptx::tma_store_wait<0>();
         __syncwarp();
+        if (p.dbg && lane == 0 && quarter == 0) {
+            p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
+            p.dbg[blockIdx.x * 8 + 6] = w_tfull;
+        }
     }
 
     __syncthreads();

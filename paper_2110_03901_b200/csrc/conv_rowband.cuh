@@ -33,6 +33,7 @@
 namespace imconv {
 
 constexpr int kMaxPairs = 8;  // S <= 16
+constexpr int kProducers = 64;  // warps 2-3 gather the planes
 
 struct RowbandParams {
     int n, h, w, k;
@@ -41,8 +42,7 @@ struct RowbandParams {
     int p_groups, q_blocks;
     long long tiles;          // n * p_groups * q_blocks
     int t_min;                // min_s floor((s*dw - pw) / sw)
-    int box_pix;              // pixels per plane TMA box (box W extent = box_pix * sw <= 256)
-    int n_boxes;              // boxes loaded per plane
+    int needed;               // plane pixels loaded per input row: min(Q,128) + t_max - t_min
     int plane_bytes;          // smem bytes per plane (covers 128 + t_max - t_min pixels)
     int a_stage_bytes;        // sw * plane_bytes
     int n_stages;
@@ -54,7 +54,18 @@ struct RowbandParams {
     int pair_lbo[kMaxPairs];    // byte distance to the second tap's run (> 0)
     int pair_s0[kMaxPairs];     // tap index (0..S-1) of the first / second half; -1 = zero tap
     int pair_s1[kMaxPairs];
+    const uint8_t *x;         // NHWC input, 16 bytes per pixel
+    long long *dbg;           // optional per-CTA wait-cycle counters (instrumentation), else nullptr
+    int dbg_flags;            // instrumentation: 1 = epilogue skips TMEM/stores, 2 = producer skips copies,
+                              // 4 = one MMA per (row, filter row) instead of npairs
 };
+
+// instrumentation: cycles spent in a blocking wait, accumulated per role
+__device__ __forceinline__ void timed_wait(uint64_t *bar, uint32_t parity, long long &acc) {
+    const long long t0 = clock64();
+    ptx::mbar_wait(bar, parity);
+    acc += clock64() - t0;
+}
 
 template <int ELEM, int OUT, int BN, int TP>
 struct RowbandCfg {
@@ -67,8 +78,8 @@ struct RowbandCfg {
 
 template <int ELEM, int OUT, int BN, int TP>
 __global__ void __launch_bounds__(kThreads, 1)
-    conv_rowband_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                        const __grid_constant__ CUtensorMap tmap_y, const RowbandParams p) {
+    conv_rowband_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_y,
+                        const RowbandParams p) {
     using Cfg = RowbandCfg<ELEM, OUT, BN, TP>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -82,16 +93,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *tempty = tfull + 2;
     uint64_t *bfull = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
+    uint64_t *adesc_tab = reinterpret_cast<uint64_t *>(tmem_slot + 2);          // kMaxPairs entries
+    int8_t *rr_tab = reinterpret_cast<int8_t *>(adesc_tab + kMaxPairs);         // in_rows * TP entries (<= 256)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
 
     if (warp == 0 && lane == 0) {
-        ptx::prefetch_tmap(&tmap_x);
         ptx::prefetch_tmap(&tmap_w);
         ptx::prefetch_tmap(&tmap_y);
         for (int i = 0; i < p.n_stages; ++i) {
-            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&full[i], kProducers);  // one arrival per plane-producer thread
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -123,78 +135,127 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tma_load_2d(smem_b + j * p.b_chunk_bytes + grp * 1024, &tmap_w, bfull, j * 64, row,
                                              pol_w);
                     }
-            // ---- input planes, one stage per input row of a block ----
-            const uint64_t pol_x = ptx::policy_evict_normal();
-            const uint32_t stage_tx = static_cast<uint32_t>(p.sw * p.n_boxes * p.box_pix * 16);
-            int stage = 0;
-            uint32_t phase = 0;
-            for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-                const int qb = static_cast<int>(tile % p.q_blocks);
-                const long long rest = tile / p.q_blocks;
-                const int pg = static_cast<int>(rest % p.p_groups);
-                const int n = static_cast<int>(rest / p.p_groups);
-                const int q0 = qb * 128;
-                const int h0 = pg * TP * p.sh - p.ph;
-                for (int i = 0; i < p.in_rows; ++i) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], stage_tx);
-                    uint8_t *dst = smem_a + stage * p.a_stage_bytes;
-                    for (int e = 0; e < p.sw; ++e)
-                        for (int b = 0; b < p.n_boxes; ++b)
-                            ptx::tma_load_4d(dst + e * p.plane_bytes + b * p.box_pix * 16, &tmap_x, &full[stage], 0,
-                                             p.sw * (q0 + p.t_min + b * p.box_pix) + e, h0 + i, n, pol_x);
-                    if (++stage == p.n_stages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-            }
         }
         __syncwarp();
-    } else if (warp == 1) {
-        // ---- MMA issuer ----
-        const uint32_t idesc = make_idesc<ELEM, BN>();
-        ptx::mbar_wait(bfull, 0);
-        const uint32_t b_base = ptx::smem_u32(smem_b);
+    } else if (warp == 2 || warp == 3) {
+        // ---- plane producers: cp.async 16-byte pixels into the stride-phase planes ----
+        // (LSU path: a 16-byte TMA element costs as much TMA time as a 128-byte
+        // one, so strided 16-byte pixels are gathered by threads instead)
+        const int t = threadIdx.x - 64;
+        const int entries = p.sw * p.needed;
+        const uint32_t a0 = ptx::smem_u32(smem_a);
+        const size_t row_bytes = static_cast<size_t>(p.w) * 16;
+        constexpr int kLag = 4;  // cp.async groups kept in flight per thread
+        int pend[kLag + 1];
+        int npend = 0;
         int stage = 0;
         uint32_t phase = 0;
-        int acc = 0;
-        uint32_t acc_phase = 0;
+        long long w_empty = 0;
+        const long long t_start = clock64();
         for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-            ptx::tc_fence_after();
-            const uint32_t d_base = tmem_base + static_cast<uint32_t>(acc * TP * BN);
+            const int qb = static_cast<int>(tile % p.q_blocks);
+            const long long rest = tile / p.q_blocks;
+            const int pg = static_cast<int>(rest % p.p_groups);
+            const int n = static_cast<int>(rest / p.p_groups);
+            const int col0 = p.sw * (qb * 128 + p.t_min);
+            const int h0 = pg * TP * p.sh - p.ph;
             for (int i = 0; i < p.in_rows; ++i) {
-                ptx::mbar_wait(&full[stage], phase);
-                ptx::tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a_base = ptx::smem_u32(smem_a + stage * p.a_stage_bytes);
-#pragma unroll
-                    for (int j = 0; j < TP; ++j) {
-                        int rr = i - j * p.sh;
-                        if (rr < 0 || rr % p.dh != 0) continue;
-                        rr /= p.dh;
-                        if (rr >= p.r) continue;
-                        for (int pr = 0; pr < p.npairs; ++pr) {
-                            const uint64_t adesc =
-                                ptx::smem_desc(a_base + p.pair_a_off[pr], p.pair_lbo[pr], 128, ptx::LAYOUT_NONE);
-                            const uint64_t bdesc = ptx::smem_desc(b_base + ((rr * p.npairs + pr) * 2) * 1024,
-                                                                  p.b_chunk_bytes, 1024, ptx::LAYOUT_SW128);
-                            ptx::mma_f16(d_base + j * BN, adesc, bdesc, idesc, (rr | pr) != 0 ? 1u : 0u);
-                        }
-                    }
-                    ptx::mma_commit(&empty[stage]);
+                timed_wait(&empty[stage], phase ^ 1, w_empty);
+                const int h = h0 + i;
+                const bool row_ok = h >= 0 && h < p.h;
+                const uint8_t *xrow = p.x + (static_cast<size_t>(n) * p.h + (row_ok ? h : 0)) * row_bytes;
+                const uint32_t dst0 = a0 + stage * p.a_stage_bytes;
+                for (int k = t; k < ((p.dbg_flags & 2) ? 0 : entries); k += kProducers) {
+                    const int e = k / p.needed;
+                    const int j = k - e * p.needed;
+                    const int col = col0 + p.sw * j + e;
+                    const bool ok = row_ok && col >= 0 && col < p.w;
+                    ptx::cp_async_16(dst0 + e * p.plane_bytes + j * 16, xrow + (ok ? col : 0) * 16, ok ? 16u : 0u);
                 }
-                __syncwarp();
+                ptx::cp_async_commit();
+                pend[npend++] = stage;
+                if (npend > kLag) {
+                    ptx::cp_async_wait<kLag>();
+                    ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05 (async proxy)
+                    ptx::mbar_arrive(&full[pend[0]]);
+                    for (int u = 0; u < kLag; ++u) pend[u] = pend[u + 1];
+                    --npend;
+                }
                 if (++stage == p.n_stages) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (lane == 0) ptx::mma_commit(&tfull[acc]);
-            __syncwarp();
+        }
+        ptx::cp_async_wait<0>();
+        ptx::fence_proxy_async_smem();
+        for (int u = 0; u < npend; ++u) ptx::mbar_arrive(&full[pend[u]]);
+        if (p.dbg && t == 0) {
+            p.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
+            p.dbg[blockIdx.x * 8 + 1] = w_empty;
+        }
+    } else if (warp == 1) {
+        // ---- MMA issuer ----
+        // Per-MMA work is two 64-bit adds: descriptors are built once (the
+        // 14-bit start-address field absorbs stage / filter-row offsets >> 4)
+        // and the (output row j, filter row r) pairs of every input row are
+        // tabulated, so the single issuing thread keeps up with N = 64 MMAs.
+        const uint32_t idesc = make_idesc<ELEM, BN>();
+        for (int u = lane; u < p.in_rows * TP; u += 32) {
+            const int i = u / TP, j = u - (u / TP) * TP;
+            int rr = i - j * p.sh;
+            rr = (rr >= 0 && rr % p.dh == 0 && rr / p.dh < p.r) ? rr / p.dh : -1;
+            rr_tab[u] = static_cast<int8_t>(rr);
+        }
+        if (lane < p.npairs)
+            adesc_tab[lane] = ptx::smem_desc(ptx::smem_u32(smem_a) + p.pair_a_off[lane], p.pair_lbo[lane], 128,
+                                             ptx::LAYOUT_NONE);
+        __syncwarp();
+        const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(smem_b), p.b_chunk_bytes, 1024, ptx::LAYOUT_SW128);
+        const int npairs = (p.dbg_flags & 4) ? 1 : p.npairs;
+        const uint32_t stage_enc = static_cast<uint32_t>(p.a_stage_bytes >> 4);
+        ptx::mbar_wait(bfull, 0);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        long long w_tempty = 0, w_full = 0;
+        const long long t_start = clock64();
+        for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            timed_wait(&tempty[acc], acc_phase ^ 1, w_tempty);
+            ptx::tc_fence_after();
+            const uint32_t d_base = tmem_base + static_cast<uint32_t>(acc * TP * BN);
+            for (int i = 0; i < p.in_rows; ++i) {
+                timed_wait(&full[stage], phase, w_full);
+                ptx::tc_fence_after();
+                {
+                    const uint64_t a_add = static_cast<uint64_t>(stage * stage_enc);
+#pragma unroll
+                    for (int j = 0; j < TP; ++j) {
+                        const int rr = rr_tab[i * TP + j];
+                        if (rr < 0) continue;  // warp-uniform
+                        const uint64_t b_row = bdesc0 + static_cast<uint64_t>(rr * npairs * 128);
+                        for (int pr = 0; pr < npairs; ++pr)
+                            ptx::mma_f16_elect(d_base + j * BN, adesc_tab[pr] + a_add,
+                                               b_row + static_cast<uint64_t>(pr * 128), idesc,
+                                               (rr | pr) != 0 ? 1u : 0u);
+                    }
+                    ptx::mma_commit_elect(&empty[stage]);
+                }
+                if (++stage == p.n_stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            ptx::mma_commit_elect(&tfull[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
+        }
+        if (p.dbg && lane == 0) {
+            p.dbg[blockIdx.x * 8 + 2] = clock64() - t_start;
+            p.dbg[blockIdx.x * 8 + 3] = w_tempty;
+            p.dbg[blockIdx.x * 8 + 4] = w_full;
+
         }
     } else if (warp >= 4) {
         // ---- epilogue: TP accumulators -> NHWC via 4-D TMA stores ----
@@ -204,13 +265,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         uint32_t chunk_ctr = 0;
+        long long w_tfull = 0;
+        const long long t_start = clock64();
         for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
             const int qb = static_cast<int>(tile % p.q_blocks);
             const long long rest = tile / p.q_blocks;
             const int pg = static_cast<int>(rest % p.p_groups);
             const int n = static_cast<int>(rest / p.p_groups);
             const int qrow = qb * 128 + quarter * 32;
-            ptx::mbar_wait(&tfull[acc], acc_phase);
+            timed_wait(&tfull[acc], acc_phase, w_tfull);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int j = 0; j < TP; ++j) {
@@ -218,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
+                    if (p.dbg_flags & 1) continue;
                     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                            static_cast<uint32_t>(acc * TP * BN + j * BN + c * 32);
                     ptx::tmem_ld_32x32b_x32(taddr, v);
@@ -244,6 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (lane == 0) ptx::tma_store_wait<0>();
         __syncwarp();
+        if (p.dbg && lane == 0 && quarter == 0) {
+            p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
+            p.dbg[blockIdx.x * 8 + 6] = w_tfull;
+        }
     }
 
     __syncthreads();

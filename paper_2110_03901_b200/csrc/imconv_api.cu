@@ -24,6 +24,8 @@ namespace imconv {
 namespace {
 
 thread_local int64_t g_launches = 0;
+long long *g_debug_buf = nullptr;  // instrumentation target (imconv_debug_set_buffer)
+int g_debug_flags = 0;
 
 std::mutex g_mu;
 PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
@@ -128,8 +130,8 @@ constexpr int kMaxDynSmem = 227 * 1024;
 inline int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 
 template <int ELEM, int OUT, int BN, int TP>
-int launch_rowband(const CUtensorMap &tx, const CUtensorMap &tw, const CUtensorMap &ty, const RowbandParams &p,
-                   int smem, int grid, cudaStream_t st) {
+int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandParams &p, int smem, int grid,
+                   cudaStream_t st) {
     auto kern = conv_rowband_kernel<ELEM, OUT, BN, TP>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -137,17 +139,19 @@ int launch_rowband(const CUtensorMap &tx, const CUtensorMap &tw, const CUtensorM
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid, kThreads, smem, st>>>(tx, tw, ty, p);
+    kern<<<grid, kThreads, smem, st>>>(tw, ty, p);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }
 
-// Row-band path for 16-byte pixels (bf16/fp16, C = 8).  Returns 1 when the
-// layer does not qualify (the caller then uses the generic kernel).
+constexpr int kNotApplicable = -1000;  // internal: layer does not qualify for a specialised path
+
+// Row-band path for 16-byte pixels (bf16/fp16, C = 8).  Returns kNotApplicable
+// when the layer does not qualify (the caller then uses the generic kernel).
 int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st) {
-    if (!(a->in_dtype == IMCONV_BF16 || a->in_dtype == IMCONV_F16) || a->c != 8) return 1;
-    if (a->tile_n != 0 || a->k > 256 || a->s > 2 * kMaxPairs || a->stride_w > 8) return 1;
+    if (!(a->in_dtype == IMCONV_BF16 || a->in_dtype == IMCONV_F16) || a->c != 8) return kNotApplicable;
+    if (a->tile_n != 0 || a->k > 256 || a->s > 2 * kMaxPairs || a->stride_w > 8) return kNotApplicable;
     const int K = static_cast<int>(a->k), R = static_cast<int>(a->r), S = static_cast<int>(a->s);
     const int BN = K <= 64 ? 64 : (K <= 128 ? 128 : 256);
     const int TP = 256 / BN;
@@ -179,10 +183,12 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
         t_max = std::max(t_max, t_s[s]);
     }
     p.t_min = t_min;
-    p.box_pix = ((256 / p.sw) / 8) * 8;
-    const int needed = static_cast<int>(std::min<int64_t>(Q, 128)) + t_max - t_min;
-    p.n_boxes = (needed + p.box_pix - 1) / p.box_pix;
-    const int plane_pix = std::max(128 + t_max - t_min, p.n_boxes * p.box_pix);
+    // +1: a pair's zero half reads the run one pixel past its first tap
+    p.needed = static_cast<int>(std::min<int64_t>(Q, 128)) + t_max - t_min + 1;
+    const int plane_pix = 129 + t_max - t_min;
+    p.x = static_cast<const uint8_t *>(a->x);
+    p.dbg = g_debug_buf;
+    p.dbg_flags = g_debug_flags;
     p.plane_bytes = ((plane_pix * 16 + 127) / 128) * 128;
     p.a_stage_bytes = p.sw * p.plane_bytes;
     p.in_rows = (TP - 1) * p.sh + (R - 1) * p.dh + 1;
@@ -205,30 +211,17 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
         p.pair_lbo[pr] = s1 >= 0 ? addr[s1] - addr[s0] : 16;  // zero tap: any finite run
     }
     const int kStageOut = 2 * 32 * ((a->out_dtype == IMCONV_F32) ? 128 : 64);
-    const int fixed = p.b_bytes + 4 * kStageOut + 1024 + 512;
+    const int fixed = p.b_bytes + 4 * kStageOut + 1024 /*align*/ + 1024 /*barriers + tables*/;
     const int room = kMaxDynSmem - fixed;
     p.n_stages = std::min(24, room / p.a_stage_bytes);
-    if (p.b_bytes > 128 * 1024 || p.n_stages < 3) return 1;
+    if (p.b_bytes > 128 * 1024 || p.n_stages < 3 || p.in_rows * TP > 256 || 2 * p.n_stages * 8 + 64 > 512)
+        return kNotApplicable;
     const int smem = fixed + p.n_stages * p.a_stage_bytes;
 
-    // plane map: tiled 4-D over NHWC with element stride sw along W
-    CUtensorMap tx, tw, ty;
-    std::memset(&tx, 0, sizeof(tx));
+    CUtensorMap tw, ty;
     std::memset(&tw, 0, sizeof(tw));
     std::memset(&ty, 0, sizeof(ty));
-    const int64_t N = a->n, H = a->h, W = a->w_, C = 8;
-    {
-        cuuint64_t gdim[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
-                              static_cast<cuuint64_t>(N)};
-        cuuint64_t gstride[3] = {static_cast<cuuint64_t>(C * 2), static_cast<cuuint64_t>(W * C * 2),
-                                 static_cast<cuuint64_t>(H * W * C * 2)};
-        cuuint32_t box[4] = {8, static_cast<cuuint32_t>(p.box_pix * p.sw), 1, 1};
-        cuuint32_t es[4] = {1, static_cast<cuuint32_t>(p.sw), 1, 1};
-        if (g_encode_tiled(&tx, tmap_dtype(a->in_dtype), 4, const_cast<void *>(a->x), gdim, gstride, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return IMCONV_ETMAP;
-    }
+    const int64_t N = a->n, C = 8;
     {
         cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(R * S * C)};
         cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * 2)};
@@ -260,9 +253,9 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     const bool f32 = a->out_dtype == IMCONV_F32;
 #define IMCONV_RB(EL, OUTK)                                                                          \
     switch (BN) {                                                                                    \
-        case 64: return launch_rowband<EL, OUTK, 64, 4>(tx, tw, ty, p, smem, grid, st);              \
-        case 128: return launch_rowband<EL, OUTK, 128, 2>(tx, tw, ty, p, smem, grid, st);            \
-        default: return launch_rowband<EL, OUTK, 256, 1>(tx, tw, ty, p, smem, grid, st);             \
+        case 64: return launch_rowband<EL, OUTK, 64, 4>(tw, ty, p, smem, grid, st);              \
+        case 128: return launch_rowband<EL, OUTK, 128, 2>(tw, ty, p, smem, grid, st);            \
+        default: return launch_rowband<EL, OUTK, 256, 1>(tw, ty, p, smem, grid, st);             \
     }
     if (a->in_dtype == IMCONV_BF16) {
         if (f32) { IMCONV_RB(ELEM_BF16, OUT_F32) } else { IMCONV_RB(ELEM_BF16, OUT_BF16) }
@@ -314,6 +307,8 @@ int imconv_device_sm_count(int32_t *sm_count) {
 }
 
 int64_t imconv_launch_count(void) { return g_launches; }
+void imconv_debug_set_buffer(void *dev_buf) { g_debug_buf = static_cast<long long *>(dev_buf); }
+void imconv_debug_set_flags(int flags) { g_debug_flags = flags; }
 void imconv_reset_launch_count(void) { g_launches = 0; }
 
 int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
@@ -354,7 +349,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
 
     if (a->order != IMCONV_ORDER_FILTER_MAJOR) {
         const int rb = try_rowband(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
-        if (rb != 1) return rb;
+        if (rb != kNotApplicable) return rb;
     }
 
     const int bn = pick_bn(a->in_dtype, K, a->tile_n);
@@ -454,6 +449,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     p.order = a->order == IMCONV_ORDER_FILTER_MAJOR ? 1 : 0;
     p.y = a->y;
     p.ldy = K;
+    p.dbg = g_debug_buf;
 
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;

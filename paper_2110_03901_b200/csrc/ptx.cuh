@@ -41,27 +41,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     asm volatile(
         "{\n\t"
         ".reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, P1;\n\t"
         "}"
         : "=r"(ok)
-        : "r"(addr), "r"(parity), "r"(0x989680)
+        : "r"(addr), "r"(parity)
         : "memory");
     return ok != 0;
 }
 
-// Blocking phase wait.  A watchdog turns a pipeline deadlock into a trap
-// (an error the host sees) instead of a hung GPU: each try_wait suspends for
-// at most ~10 ms, so the bound is tens of seconds -- far beyond any
-// legitimate wait inside one launch.
-#ifndef IMCONV_WATCHDOG_TRIES
-#define IMCONV_WATCHDOG_TRIES 4000u
-#endif
+// Blocking phase wait (no suspend-time hint: a hinted try_wait compiles to a
+// NANOSLEEP loop that wakes late).  A watchdog turns a pipeline deadlock into
+// a trap -- an error the host sees -- instead of a hung GPU: after ~2^34
+// cycles (~9 s) of waiting on one phase, far beyond any legitimate wait.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
+    if (mbar_try_wait(addr, parity)) return;
+    const long long t0 = clock64();
     uint32_t tries = 0;
     while (!mbar_try_wait(addr, parity)) {
-        if (++tries > IMCONV_WATCHDOG_TRIES) __trap();
+        if ((++tries & 1023u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
     }
 }
 
@@ -146,6 +145,19 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- cp.async (LSU path)
+// 16-byte global -> shared copy through L1 (.ca: the neighbouring stride phase
+// of the same lines is read by the next instruction); src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp_async_16(uint32_t dst_smem, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem) {
@@ -181,6 +193,37 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Warp-collective forms: every lane executes the instruction with identical
+// (warp-uniform) operands and elect.sync picks the single issuing lane inside
+// the asm, so descriptor arithmetic stays in uniform registers.
+__device__ __forceinline__ void mma_f16_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_i8_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
         : "memory");
 }
 

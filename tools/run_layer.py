@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--tile-n", type=int, default=0)
     ap.add_argument("--order", default="reuse_aware")
     ap.add_argument("--explicit", action="store_true", help="K3 im2col + K4 GEMM instead of the implicit kernel")
+    ap.add_argument("--waits", action="store_true", help="print per-role wait-cycle instrumentation")
+    ap.add_argument("--dbg-flags", type=int, default=0, help="instrumentation: disable kernel roles (wrong results)")
     args = ap.parse_args()
 
     import torch
@@ -39,6 +41,7 @@ def main():
         x = torch.randn((sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev).to(torch.bfloat16)
         w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev) * 0.05).to(torch.bfloat16)
     order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[args.order]
+    _lib.lib.imconv_debug_set_flags(args.dbg_flags)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for i in range(args.reps + 1):
         if i == 1:
@@ -52,6 +55,16 @@ def main():
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / args.reps
     print(f"{args.layer} n={sp.n}: {ms:.4f} ms  {sp.flops / ms / 1e9:.1f} TFLOP/s")
+    if args.waits:
+        dbg = torch.zeros(148 * 8, dtype=torch.int64, device=dev)
+        _lib.lib.imconv_debug_set_buffer(dbg.data_ptr())
+        conv_device(x, w, *sp.conv_args(), tile_n=args.tile_n, order=order)
+        torch.cuda.synchronize()
+        _lib.lib.imconv_debug_set_buffer(None)
+        d = dbg.view(148, 8).double().mean(0).tolist()
+        names = ["prod_total", "prod_wait_empty", "mma_total", "mma_wait_tempty", "mma_wait_full",
+                 "epi_total", "epi_wait_tfull", "-"]
+        print("  ".join(f"{nm}={v / 1e3:.1f}k" for nm, v in zip(names, d)))
 
 
 if __name__ == "__main__":
