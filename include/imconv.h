@@ -51,6 +51,10 @@ extern "C" {
 #define IMCONV_ORDER_REUSE_AWARE 0  /* channel chunk outer, filter tap inner (default) */
 #define IMCONV_ORDER_FILTER_MAJOR 1 /* filter tap outer, channel chunk inner          */
 
+/* imconv_conv_args.flags */
+#define IMCONV_FLAG_SINGLE_CTA 1  /* never use CTA pairs (cta_group::2)        */
+#define IMCONV_FLAG_CTA_PAIR 2    /* use CTA pairs whenever the shape allows   */
+
 /*
  * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,
  * zero padding (virtual) and dilation per axis.
@@ -87,7 +91,7 @@ typedef struct imconv_conv_args {
     int32_t tile_n;
     int32_t num_ctas;
     int32_t order;         /* IMCONV_ORDER_* */
-    int32_t reserved;
+    int32_t flags;         /* IMCONV_FLAG_*: block-shape overrides (0 = automatic) */
 } imconv_conv_args;
 
 IMCONV_API int imconv_conv2d_nhwc(const imconv_conv_args *args, void *stream);

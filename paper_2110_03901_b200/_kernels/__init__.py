@@ -81,7 +81,8 @@ def _check_int8(t: torch.Tensor, what: str):
 
 def conv_device(xd: torch.Tensor, wd: torch.Tensor, sh=1, sw=1, ph=0, pw=0, dh=1, dw=1, *,
                 out_dtype: torch.dtype | None = None, tile_n: int = 0, num_ctas: int = 0,
-                order: int = _lib.ORDER_REUSE_AWARE, y: torch.Tensor | None = None) -> torch.Tensor:
+                order: int = _lib.ORDER_REUSE_AWARE, y: torch.Tensor | None = None,
+                flags: int = 0) -> torch.Tensor:
     """Core device call: CUDA tensors already in the compute dtype
     (bf16 / f16 / int8), x (N,H,W,C), w (R,S,C,K) -> y (N,P,Q,K)."""
     if xd.dim() != 4 or wd.dim() != 4:
@@ -120,7 +121,7 @@ def conv_device(xd: torch.Tensor, wd: torch.Tensor, sh=1, sw=1, ph=0, pw=0, dh=1
     a.n, a.h, a.w_, a.c = n, h, wi, c_pad
     a.k, a.r, a.s = k_pad, r, s
     a.stride_h, a.stride_w, a.pad_h, a.pad_w, a.dil_h, a.dil_w = sh, sw, ph, pw, dh, dw
-    a.tile_n, a.num_ctas, a.order = tile_n, num_ctas, order
+    a.tile_n, a.num_ctas, a.order, a.flags = tile_n, num_ctas, order, flags
     _lib.check(_lib.lib.imconv_conv2d_nhwc(a, D.stream_handle()), "imconv_conv2d_nhwc")
     if k_pad != k:
         yk = yk[..., :k].contiguous()
@@ -131,7 +132,7 @@ def conv_device(xd: torch.Tensor, wd: torch.Tensor, sh=1, sw=1, ph=0, pw=0, dh=1
 
 
 def conv2d_nhwc(x, w, sh, sw, ph, pw, dh, dw, *, compute: str | None = None, out_dtype=None,
-                tile_n: int = 0, num_ctas: int = 0, order: str = "reuse_aware"):
+                tile_n: int = 0, num_ctas: int = 0, order: str = "reuse_aware", flags: int = 0):
     """Direct convolution NHWC x HWCN -> NHWC with virtual zero padding.
 
     Drop-in for the reference's ``conv2d_nhwc(x, w, sh, sw, ph, pw, dh, dw)``
@@ -146,7 +147,8 @@ def conv2d_nhwc(x, w, sh, sw, ph, pw, dh, dw, *, compute: str | None = None, out
         _check_int8(xd, "input")
         _check_int8(wd, "filter")
     xd, wd = xd.to(cdt), wd.to(cdt)
-    y = conv_device(xd, wd, sh, sw, ph, pw, dh, dw, out_dtype=odt, tile_n=tile_n, num_ctas=num_ctas, order=ordc)
+    y = conv_device(xd, wd, sh, sw, ph, pw, dh, dw, out_dtype=odt, tile_n=tile_n, num_ctas=num_ctas, order=ordc,
+                    flags=flags)
     if np_res is not None and not D.is_device_array(x):
         return D.to_host(y, np_res)
     return y

@@ -10,11 +10,15 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libimconv.so")
+# IMCONV_INSTRUMENTED=1 (tools/run_layer.py --waits) loads the same sources built
+# with per-role wait counters; it is not a different backend.
+LIB_PATH = os.path.join(_PKG, "libimconv_instr.so" if os.environ.get("IMCONV_INSTRUMENTED") == "1"
+                        else "libimconv.so")
 
 # element-type codes, include/imconv.h
 BF16, F16, I8, F32, I32 = 0, 1, 2, 3, 4
 ORDER_REUSE_AWARE, ORDER_FILTER_MAJOR = 0, 1
+FLAG_SINGLE_CTA, FLAG_CTA_PAIR = 1, 2
 
 # every symbol include/imconv.h declares (checked by tests/test_abi.py)
 EXPORTED = (
@@ -37,7 +41,7 @@ class ImconvArgs(ctypes.Structure):
         ("pad_h", ctypes.c_int32), ("pad_w", ctypes.c_int32),
         ("dil_h", ctypes.c_int32), ("dil_w", ctypes.c_int32),
         ("tile_n", ctypes.c_int32), ("num_ctas", ctypes.c_int32),
-        ("order", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("order", ctypes.c_int32), ("flags", ctypes.c_int32),
     ]
 
 

@@ -17,8 +17,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libimconv.so")
+LIB_INSTR = os.path.join(PKG, "libimconv_instr.so")  # same sources, -DIMCONV_INSTRUMENT=1 (tools only)
 SOURCES = [os.path.join(CSRC, f) for f in ("imconv_api.cu", "lru.cpp")]
-HEADERS = [os.path.join(CSRC, f) for f in ("ptx.cuh", "conv_kernel.cuh", "aux_kernels.cuh")] + [
+HEADERS = [os.path.join(CSRC, f) for f in ("ptx.cuh", "conv_kernel.cuh", "conv_kernel_2sm.cuh", "conv_rowband.cuh", "aux_kernels.cuh")] + [
     os.path.join(ROOT, "include", "imconv.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -27,24 +28,26 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-cudart", "static"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    cmd = [NVCC] + ARCH + FLAGS + ["-I", os.path.join(ROOT, "include"), "-shared", "-o", LIB] + SOURCES
+def build(force: bool = False, verbose: bool = False, instrument: bool = False) -> str:
+    lib = LIB_INSTR if instrument else LIB
+    if not force and not _stale(lib):
+        return lib
+    cmd = [NVCC] + ARCH + FLAGS + ["-I", os.path.join(ROOT, "include"), "-shared", "-o", lib] + SOURCES
+    if instrument:
+        cmd.insert(1, "-DIMCONV_INSTRUMENT=1")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force=True, verbose="-v" in sys.argv, instrument="--instrument" in sys.argv))

@@ -63,12 +63,52 @@ struct ConvParams {
     void *y;
     long long ldy;       // = k
     long long *dbg;      // optional per-CTA role / wait-cycle counters (instrumentation), else nullptr
+    int b_3d;            // 1: the filter map is 3-D {chunk cols, rows, chunks}: one TMA per stage for all of B
 };
 
+// Division-free walk over the k-subtiles (filter tap <r,s>, channel chunk) of
+// one output block, in the order of blocksched.order_subtiles: REUSE_AWARE =
+// chunk outer / tap inner, FILTER_MAJOR = tap outer / chunk inner.  (The
+// producer thread's per-stage instruction latency, not TMA bandwidth, bounds
+// the pipeline -- tools/tma_bench.cu -- so no runtime divisions here.)
+struct KWalk {
+    int chunk, r, s, tap;
+    __device__ __forceinline__ void reset() { chunk = r = s = tap = 0; }
+    __device__ __forceinline__ void next(int order, int R, int S, int c_chunks) {
+        if (order == 0) {
+            ++tap;
+            if (++s == S) {
+                s = 0;
+                if (++r == R) {
+                    r = 0;
+                    tap = 0;
+                    ++chunk;
+                }
+            }
+        } else {
+            if (++chunk == c_chunks) {
+                chunk = 0;
+                ++tap;
+                if (++s == S) {
+                    s = 0;
+                    ++r;
+                }
+            }
+        }
+    }
+};
+
+// Instrumentation (IMCONV_INSTRUMENT builds only, libimconv_instr.so): cycles
+// spent in blocking waits per role; production builds compile to a plain wait.
 __device__ __forceinline__ void timed_wait_g(uint64_t *bar, uint32_t parity, long long &acc) {
+#if IMCONV_INSTRUMENT
     const long long t0 = clock64();
     ptx::mbar_wait(bar, parity);
     acc += clock64() - t0;
+#else
+    (void)acc;
+    ptx::mbar_wait(bar, parity);
+#endif
 }
 
 template <int ELEM>
@@ -184,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmap_b);
         ptx::prefetch_tmap(&tmap_y);
         for (int i = 0; i < STAGES; ++i) {
-            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&full[i], 2);  // A producer + B producer
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -199,16 +239,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
-        // ===================== TMA producer: operand generation =====================
+    if (warp == 0 || warp == 3) {
+        // ============ TMA producers: warp 0 = activations (im2col), warp 3 = filter ============
+        // Two issuing threads so A and B loads leave the SM in parallel; each
+        // arms the stage's `full` barrier with its own byte count.
         if (lane == 0) {
-            const uint64_t pol_a = ptx::policy_evict_normal();
-            const uint64_t pol_b = ptx::policy_evict_last();  // filters are re-read by every block
+            const bool is_a = warp == 0;
+            const uint64_t pol = is_a ? ptx::policy_evict_normal() : ptx::policy_evict_last();
             const int pq = p.p * p.q;
             int stage = 0;
             uint32_t phase = 0;
             long long w_empty = 0;
             const long long t_start = clock64();
+            KWalk kw;
             for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
                 const long long m_tile = tile / p.n_tiles;
                 const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
@@ -220,52 +263,62 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int w0 = q0 * p.sw - p.pw;  // base pixel (im2col bounding-box coordinates)
                 const int h0 = p0 * p.sh - p.ph;
                 const int nb0 = n_tile * BN;
+                kw.reset();
                 for (int kb = 0; kb < p.k_stages; ++kb) {
                     timed_wait_g(&empty[stage], phase ^ 1, w_empty);
-                    ptx::mbar_arrive_expect_tx(&full[stage], kAStage + Cfg::kBStage);
-                    uint8_t *a_dst = smem_a + stage * kAStage;
-                    uint8_t *b_dst = smem_b + stage * Cfg::kBStage;
-                    int brow;
+                    ptx::mbar_arrive_expect_tx(&full[stage], is_a ? kAStage : Cfg::kBStage);
                     if (p.tps == 1) {
-                        int chunk, tap;
-                        if (p.order == 0) {
-                            chunk = kb / p.rs;
-                            tap = kb - chunk * p.rs;
+                        const int c0 = kw.chunk * Cfg::kBKE;
+                        if (is_a) {
+                            ptx::tma_load_im2col_4d(smem_a + stage * kAStage, &tmap_a, &full[stage], c0, w0, h0, n0,
+                                                    static_cast<uint16_t>(kw.s * p.dw),
+                                                    static_cast<uint16_t>(kw.r * p.dh), pol);
                         } else {
-                            tap = kb / p.c_chunks;
-                            chunk = kb - tap * p.c_chunks;
+                            const int brow = kw.tap * p.c + c0;
+                            uint8_t *b_dst = smem_b + stage * Cfg::kBStage;
+                            if (p.b_3d) {
+                                ptx::tma_load_3d(b_dst, &tmap_b, &full[stage], 0, brow, nb0 / Cfg::kNC, pol);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < BN / Cfg::kNC; ++j)
+                                    ptx::tma_load_2d(b_dst + j * (Cfg::kBKE * kRowBytes), &tmap_b, &full[stage],
+                                                     nb0 + j * Cfg::kNC, brow, pol);
+                            }
                         }
-                        const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
-                        const int c0 = chunk * Cfg::kBKE;
-                        ptx::tma_load_im2col_4d(a_dst, &tmap_a, &full[stage], c0, w0, h0, n0,
-                                                static_cast<uint16_t>(s * p.dw), static_cast<uint16_t>(r * p.dh),
-                                                pol_a);
-                        brow = tap * p.c + c0;
+                        kw.next(p.order, p.r, p.s, p.c_chunks);
                     } else {
                         // small-C layers: pack tps taps side by side along the
                         // reduction (the paper's multi-tile packing, §4.2)
                         const int tap0 = kb * p.tps;
-                        const int blk = kAStage / p.tps;
-                        for (int t = 0; t < p.tps; ++t) {
-                            const int tap = min(tap0 + t, p.rs - 1);  // past-the-end taps meet zero filter rows
-                            const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
-                            ptx::tma_load_im2col_4d(a_dst + t * blk, &tmap_a, &full[stage], 0, w0, h0, n0,
-                                                    static_cast<uint16_t>(s * p.dw),
-                                                    static_cast<uint16_t>(r * p.dh), pol_a);
-                        }
-                        brow = tap0 * p.c;
-                    }
+                        if (is_a) {
+                            const int blk = kAStage / p.tps;
+                            for (int t = 0; t < p.tps; ++t) {
+                                const int tap = min(tap0 + t, p.rs - 1);  // past-the-end taps meet zero filter rows
+                                const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
+                                ptx::tma_load_im2col_4d(smem_a + stage * kAStage + t * blk, &tmap_a, &full[stage], 0,
+                                                        w0, h0, n0, static_cast<uint16_t>(s * p.dw),
+                                                        static_cast<uint16_t>(r * p.dh), pol);
+                            }
+                        } else {
+                            const int brow = tap0 * p.c;
+                            uint8_t *b_dst = smem_b + stage * Cfg::kBStage;
+                            if (p.b_3d) {
+                                ptx::tma_load_3d(b_dst, &tmap_b, &full[stage], 0, brow, nb0 / Cfg::kNC, pol);
+                            } else {
 #pragma unroll
-                    for (int j = 0; j < BN / Cfg::kNC; ++j)
-                        ptx::tma_load_2d(b_dst + j * (Cfg::kBKE * kRowBytes), &tmap_b, &full[stage],
-                                         nb0 + j * Cfg::kNC, brow, pol_b);
+                                for (int j = 0; j < BN / Cfg::kNC; ++j)
+                                    ptx::tma_load_2d(b_dst + j * (Cfg::kBKE * kRowBytes), &tmap_b, &full[stage],
+                                                     nb0 + j * Cfg::kNC, brow, pol);
+                            }
+                        }
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
             }
-            if (p.dbg) {
+            if (IMCONV_INSTRUMENT && p.dbg && is_a) {
                 p.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
                 p.dbg[blockIdx.x * 8 + 1] = w_empty;
             }
@@ -311,8 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < p.k_stages; ++kb) {
                 timed_wait_g(&full[stage], phase, w_full);
                 ptx::tc_fence_after();
-                {
-                    // warp-collective issue: uniform descriptors, elect.sync inside the asm
+                if (lane == 0) {
                     const uint64_t a_st = adesc0 + static_cast<uint64_t>((stage * kAStage) >> 4);
                     const uint64_t b_st = bdesc0 + static_cast<uint64_t>((stage * Cfg::kBStage) >> 4);
 #pragma unroll
@@ -321,22 +373,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t bdesc = b_st + static_cast<uint64_t>((kk * Cfg::kMmaK * kRowBytes) >> 4);
                         const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
                         if constexpr (ELEM == ELEM_I8)
-                            ptx::mma_i8_elect(d_tmem, adesc, bdesc, idesc, accum);
+                            ptx::mma_i8(d_tmem, adesc, bdesc, idesc, accum);
                         else
-                            ptx::mma_f16_elect(d_tmem, adesc, bdesc, idesc, accum);
+                            ptx::mma_f16(d_tmem, adesc, bdesc, idesc, accum);
                     }
-                    ptx::mma_commit_elect(&empty[stage]);  // frees the smem slot once these MMAs retire
+                    ptx::mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
                 }
+                __syncwarp();
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            ptx::mma_commit_elect(&tfull[acc]);  // accumulator complete -> epilogue
+            if (lane == 0) ptx::mma_commit(&tfull[acc]);  // accumulator complete -> epilogue
+            __syncwarp();
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if (p.dbg && lane == 0) {
+        if (IMCONV_INSTRUMENT && p.dbg && lane == 0) {
             p.dbg[blockIdx.x * 8 + 2] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 3] = w_tempty;
             p.dbg[blockIdx.x * 8 + 4] = w_full;
@@ -386,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (lane == 0) ptx::tma_store_wait<0>();
         __syncwarp();
-        if (p.dbg && lane == 0 && quarter == 0) {
+        if (IMCONV_INSTRUMENT && p.dbg && lane == 0 && quarter == 0) {
             p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 6] = w_tfull;
         }

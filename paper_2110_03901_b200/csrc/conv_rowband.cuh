@@ -62,9 +62,14 @@ struct RowbandParams {
 
 // instrumentation: cycles spent in a blocking wait, accumulated per role
 __device__ __forceinline__ void timed_wait(uint64_t *bar, uint32_t parity, long long &acc) {
+#if IMCONV_INSTRUMENT
     const long long t0 = clock64();
     ptx::mbar_wait(bar, parity);
     acc += clock64() - t0;
+#else
+    (void)acc;
+    ptx::mbar_wait(bar, parity);
+#endif
 }
 
 template <int ELEM, int OUT, int BN, int TP>
@@ -165,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool row_ok = h >= 0 && h < p.h;
                 const uint8_t *xrow = p.x + (static_cast<size_t>(n) * p.h + (row_ok ? h : 0)) * row_bytes;
                 const uint32_t dst0 = a0 + stage * p.a_stage_bytes;
-                for (int k = t; k < ((p.dbg_flags & 2) ? 0 : entries); k += kProducers) {
+                for (int k = t; k < ((IMCONV_INSTRUMENT && (p.dbg_flags & 2)) ? 0 : entries); k += kProducers) {
                     const int e = k / p.needed;
                     const int j = k - e * p.needed;
                     const int col = col0 + p.sw * j + e;
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::cp_async_wait<0>();
         ptx::fence_proxy_async_smem();
         for (int u = 0; u < npend; ++u) ptx::mbar_arrive(&full[pend[u]]);
-        if (p.dbg && t == 0) {
+        if (IMCONV_INSTRUMENT && p.dbg && t == 0) {
             p.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 1] = w_empty;
         }
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ptx::LAYOUT_NONE);
         __syncwarp();
         const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(smem_b), p.b_chunk_bytes, 1024, ptx::LAYOUT_SW128);
-        const int npairs = (p.dbg_flags & 4) ? 1 : p.npairs;
+        const int npairs = (IMCONV_INSTRUMENT && (p.dbg_flags & 4)) ? 1 : p.npairs;
         const uint32_t stage_enc = static_cast<uint32_t>(p.a_stage_bytes >> 4);
         ptx::mbar_wait(bfull, 0);
         int stage = 0;
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if (p.dbg && lane == 0) {
+        if (IMCONV_INSTRUMENT && p.dbg && lane == 0) {
             p.dbg[blockIdx.x * 8 + 2] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 3] = w_tempty;
             p.dbg[blockIdx.x * 8 + 4] = w_full;
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
-                    if (p.dbg_flags & 1) continue;
+                    if (IMCONV_INSTRUMENT && (p.dbg_flags & 1)) continue;
                     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                            static_cast<uint32_t>(acc * TP * BN + j * BN + c * 32);
                     ptx::tmem_ld_32x32b_x32(taddr, v);
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (lane == 0) ptx::tma_store_wait<0>();
         __syncwarp();
-        if (p.dbg && lane == 0 && quarter == 0) {
+        if (IMCONV_INSTRUMENT && p.dbg && lane == 0 && quarter == 0) {
             p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 6] = w_tfull;
         }

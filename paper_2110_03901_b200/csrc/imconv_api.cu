@@ -18,6 +18,7 @@
 #include "../../include/imconv.h"
 #include "aux_kernels.cuh"
 #include "conv_kernel.cuh"
+#include "conv_kernel_2sm.cuh"
 #include "conv_rowband.cuh"
 
 namespace imconv {
@@ -97,6 +98,35 @@ int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap 
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+template <int ELEM, int OUT, int BN, int STAGES>
+int launch_conv_2sm(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const ConvParams &p,
+                    int grid, cudaStream_t st) {
+    using Cfg = Conv2smCfg<ELEM, OUT, BN, STAGES>;
+    auto kern = conv_fwd_2sm_kernel<ELEM, OUT, BN, STAGES>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    });
+    if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
+    kern<<<grid & ~1, kThreads, Cfg::kSmemBytes, st>>>(ta, tb, ty, p);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+template <int ELEM, int OUT>
+int dispatch_bn_2sm(int bn, const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty,
+                    const ConvParams &p, int grid, cudaStream_t st) {
+    if constexpr (ELEM == ELEM_I8) {
+        if (bn == 256) return launch_conv_2sm<ELEM, OUT, 256, 6>(ta, tb, ty, p, grid, st);
+    } else {
+        if (bn == 128) return launch_conv_2sm<ELEM, OUT, 128, 8>(ta, tb, ty, p, grid, st);
+        if (bn == 256) return launch_conv_2sm<ELEM, OUT, 256, 6>(ta, tb, ty, p, grid, st);
+    }
+    return IMCONV_EINVAL;
 }
 
 // BN -> pipeline depth that fits ~200 KB of shared memory.
@@ -390,16 +420,46 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         if (g_driver_version <= 13010 && N * H * W * C * E < 131072)
             reinterpret_cast<uint64_t *>(&ta)[1] &= ~(1ull << 21);
     }
-    // ---- B operand: tiled map over the HWCN filter viewed as (R*S*C, K) ----
+    // ---- block shape: single CTA or CTA pair (cta_group::2, B split across the pair) ----
+    // pairs need whole swizzle-atom columns per CTA (BN >= 128 bf16 / 256 int8)
+    // and enough 256-row blocks to fill the clusters.
+    const int64_t m_tiles_ = (M + kBM - 1) / kBM;
+    const int64_t n_tiles_ = (K + bn - 1) / bn;
+    const long long pair_tiles = ((m_tiles_ + 1) / 2) * n_tiles_;
+    const bool pair_ok = (a->in_dtype == IMCONV_I8) ? bn == 256 : bn >= 128;
+    // Measured (tools/run_layer.py --flags 1/2): once the producers issue one
+    // TMA per operand per stage, single CTAs match or beat pairs on the
+    // ResNet-50 shapes, so pairs are opt-in for now.
+    const bool use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && (a->flags & IMCONV_FLAG_CTA_PAIR) &&
+                          pair_tiles >= 1;
+
+    // ---- B operand: the HWCN filter as (R*S*C rows, K cols).  When K is a whole
+    // number of 128-byte column chunks it is viewed 3-D {chunk cols, rows, chunks}
+    // so ONE TMA instruction fetches all of a stage's B chunks. ----
+    const int nc = kRowBytes / E;
+    const bool b_3d = (K % nc) == 0;
     {
-        const int nc = kRowBytes / E;
-        cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(R * S * C)};
-        cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * E)};
-        cuuint32_t box[2] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(kRowBytes / E)};
-        cuuint32_t estride[2] = {1, 1};
-        CUresult cr = g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 2, const_cast<void *>(a->w), gdim, gstride, box,
-                                     estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const int chunks_per_load = (use_pair ? bn / 2 : bn) / nc;
+        CUresult cr;
+        if (b_3d) {
+            cuuint64_t gdim[3] = {static_cast<cuuint64_t>(nc), static_cast<cuuint64_t>(R * S * C),
+                                  static_cast<cuuint64_t>(K / nc)};
+            cuuint64_t gstride[2] = {static_cast<cuuint64_t>(K * E), static_cast<cuuint64_t>(nc * E)};
+            cuuint32_t box[3] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(kRowBytes / E),
+                                 static_cast<cuuint32_t>(chunks_per_load)};
+            cuuint32_t estride[3] = {1, 1, 1};
+            cr = g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 3, const_cast<void *>(a->w), gdim, gstride, box,
+                                estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        } else {
+            cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(R * S * C)};
+            cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * E)};
+            cuuint32_t box[2] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(kRowBytes / E)};
+            cuuint32_t estride[2] = {1, 1};
+            cr = g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 2, const_cast<void *>(a->w), gdim, gstride, box,
+                                estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        }
         if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
     }
 
@@ -450,12 +510,29 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     p.y = a->y;
     p.ldy = K;
     p.dbg = g_debug_buf;
+    p.b_3d = b_3d ? 1 : 0;
 
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
-    if (grid > tiles) grid = static_cast<int>(tiles);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 
+    if (use_pair) {
+        int g2 = grid;
+        if (g2 > 2 * pair_tiles) g2 = static_cast<int>(2 * pair_tiles);
+        if (g2 < 2) g2 = 2;
+        switch (a->in_dtype) {
+            case IMCONV_BF16:
+                return a->out_dtype == IMCONV_F32 ? dispatch_bn_2sm<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
+                                                  : dispatch_bn_2sm<ELEM_BF16, OUT_BF16>(bn, ta, tb, ty, p, g2, st);
+            case IMCONV_F16:
+                return a->out_dtype == IMCONV_F32 ? dispatch_bn_2sm<ELEM_F16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
+                                                  : dispatch_bn_2sm<ELEM_F16, OUT_F16>(bn, ta, tb, ty, p, g2, st);
+            case IMCONV_I8: return dispatch_bn_2sm<ELEM_I8, OUT_I32>(bn, ta, tb, ty, p, g2, st);
+            default: return IMCONV_EDTYPE;
+        }
+    }
+
+    if (grid > tiles) grid = static_cast<int>(tiles);
     switch (a->in_dtype) {
         case IMCONV_BF16:
             return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, grid, st)

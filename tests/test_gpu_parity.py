@@ -263,3 +263,32 @@ def test_resnet50_layers_reduced_batch():
             continue
         seen.add(key)
         _layer_check(layer)
+
+
+@pytest.mark.parametrize("flags", [1, 2])
+def test_cta_pair_parity(rng, flags):
+    """CTA pairs (cta_group::2, B split across the pair) vs single CTAs:
+    identical integer results, ragged 256-row blocks, odd grids."""
+    P = _P()
+    from oracle import oracle as O
+    cases = [((3, 13, 11, 64), (3, 3, 64, 128), (1, 2, 1, 1, 2, 1)),
+             ((2, 17, 9, 128), (1, 1, 128, 256), (1, 1, 0, 0, 1, 1)),
+             ((1, 30, 30, 64), (3, 3, 64, 200), (2, 2, 1, 1, 1, 1)),
+             ((2, 9, 9, 8), (5, 5, 8, 384), (1, 1, 2, 2, 1, 1))]
+    for xs, ws, args in cases:
+        x = rng.integers(-4, 5, size=xs).astype(np.int64)
+        w = rng.integers(-4, 5, size=ws).astype(np.int64)
+        want = O.conv2d_nhwc_i64(x, w, *args).astype(np.float32)
+        xb = torch.from_numpy(x).float().cuda().bfloat16()
+        wb = torch.from_numpy(w).float().cuda().bfloat16()
+        for ctas in (0, 2, 6):
+            y = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32, num_ctas=ctas, flags=flags,
+                                       tile_n=256 if ws[3] > 128 else 0)
+            assert np.array_equal(y.cpu().numpy(), want), (xs, ws, ctas)
+    # int8 pairs (BN = 256)
+    x = rng.integers(-128, 128, size=(2, 14, 14, 256)).astype(np.int8)
+    w = rng.integers(-128, 128, size=(3, 3, 256, 256)).astype(np.int8)
+    want = O.conv2d_nhwc_exact_f64(x, w, 1, 1, 1, 1, 1, 1)
+    y = P._kernels.conv2d_nhwc(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), 1, 1, 1, 1, 1, 1,
+                               flags=flags)
+    assert np.array_equal(y.cpu().numpy(), want)

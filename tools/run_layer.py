@@ -18,10 +18,13 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--tile-n", type=int, default=0)
     ap.add_argument("--order", default="reuse_aware")
+    ap.add_argument("--flags", type=int, default=0, help="imconv flags: 1 = single CTA, 2 = CTA pair")
     ap.add_argument("--explicit", action="store_true", help="K3 im2col + K4 GEMM instead of the implicit kernel")
     ap.add_argument("--waits", action="store_true", help="print per-role wait-cycle instrumentation")
     ap.add_argument("--dbg-flags", type=int, default=0, help="instrumentation: disable kernel roles (wrong results)")
     args = ap.parse_args()
+    if args.waits or args.dbg_flags:
+        os.environ["IMCONV_INSTRUMENTED"] = "1"
 
     import torch
     from paper_2110_03901_b200 import _lib
@@ -50,7 +53,7 @@ def main():
             low = K.im2col_nhwc(x, sp.h_f, sp.w_f, *sp.conv_args(), True)
             gemm_device(low, w.reshape(-1, sp.c_o))
         else:
-            conv_device(x, w, *sp.conv_args(), tile_n=args.tile_n, order=order)
+            conv_device(x, w, *sp.conv_args(), tile_n=args.tile_n, order=order, flags=args.flags)
     ev[1].record()
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / args.reps
