@@ -120,9 +120,8 @@ def dist_setup():
 
 def shard_batch(n_total: int, world: int, rank: int):
     """Even N-sharding; ranks get contiguous image ranges."""
-    base, extra = divmod(n_total, world)
-    lo = rank * base + min(rank, extra)
-    return lo, lo + base + (1 if rank < extra else 0)
+    from paper_2110_03901_b200.sharding import shard_range
+    return shard_range(n_total, world, rank)
 
 
 def cpu_threads():
