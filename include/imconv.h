@@ -54,6 +54,8 @@ extern "C" {
 /* imconv_conv_args.flags */
 #define IMCONV_FLAG_SINGLE_CTA 1  /* never use CTA pairs (cta_group::2)        */
 #define IMCONV_FLAG_CTA_PAIR 2    /* use CTA pairs whenever the shape allows   */
+#define IMCONV_FLAG_KSUB1 4       /* one k-subtile per pipeline stage (N<=128 default is 2) */
+#define IMCONV_FLAG_MT1 8         /* one 128-pixel m-tile per CTA (N<=128 default is two)  */
 
 /*
  * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,

@@ -41,6 +41,7 @@ constexpr int kBM = 128;           // output pixels per block (MMA M)
 constexpr int kRowBytes = 128;     // bytes of reduction per stage per row (one 128B swizzle span)
 constexpr int kAStage = kBM * kRowBytes;  // 16 KiB of A per stage
 constexpr int kThreads = 256;
+constexpr int kThreadsGeneric = 288;  // + warp 8: second filter producer
 
 enum ElemKind : int { ELEM_BF16 = 0, ELEM_F16 = 1, ELEM_I8 = 2 };
 enum OutKind : int { OUT_BF16 = 0, OUT_F16 = 1, OUT_F32 = 2, OUT_I32 = 3 };
@@ -183,32 +184,80 @@ __device__ __forceinline__ void stage_row_chunk(uint8_t *buf, uint32_t row, cons
     }
 }
 
-template <int ELEM, int OUT, int BN, int STAGES>
+// One 128-byte row of a 128-row output staging tile in the SW128 TMA layout
+// (16-byte chunk c of row r lives at ((c ^ (r & 7)) * 16)): 64 bf16/fp16 or
+// 32 fp32/int32 accumulator columns.
+template <int OUT>
+__device__ __forceinline__ void stage_row128(uint8_t *tile, uint32_t row, const uint32_t *v) {
+    uint8_t *dst = tile + row * 128;
+    const uint32_t swz = row & 7;
+    if constexpr (OUT == OUT_BF16 || OUT == OUT_F16) {
+#pragma unroll
+        for (uint32_t c = 0; c < 8; ++c) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float a = __uint_as_float(v[8 * c + 2 * i]), b = __uint_as_float(v[8 * c + 2 * i + 1]);
+                if constexpr (OUT == OUT_BF16) {
+                    __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+                    w[i] = *reinterpret_cast<uint32_t *>(&t);
+                } else {
+                    __half2 t = __floats2half2_rn(a, b);
+                    w[i] = *reinterpret_cast<uint32_t *>(&t);
+                }
+            }
+            *reinterpret_cast<uint4 *>(dst + ((c ^ swz) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    } else {
+#pragma unroll
+        for (uint32_t c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4 *>(dst + ((c ^ swz) << 4)) =
+                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    }
+}
+
+template <int ELEM, int OUT, int BN, int STAGES, int KSUB = 1, int MT = 1>
 struct ConvCfg {
     static constexpr int kE = ElemTraits<ELEM>::kBytes;
-    static constexpr int kBKE = kRowBytes / kE;      // reduction elements per stage
+    static constexpr int kBKE = kRowBytes / kE;      // reduction elements per k-subtile
     static constexpr int kNC = kRowBytes / kE;       // n-chunk of one MN-major SW128 atom column
-    static constexpr int kBStage = BN * kRowBytes;   // bytes of B per stage
+    static constexpr int kRows = MT * kBM;           // output pixels per CTA block (MT accumulators)
+    static constexpr int kASub = MT * kAStage;       // bytes of A per k-subtile (one im2col box of kRows pixels)
+    static constexpr int kBSub = BN * kRowBytes;     // bytes of B per k-subtile
+    static constexpr int kAStageK = KSUB * kASub;    // a pipeline stage carries KSUB k-subtiles
+    static constexpr int kBStage = KSUB * kBSub;
     static constexpr int kMmaK = 32 / kE;            // reduction elements per tcgen05.mma
-    static constexpr int kMmaPerStage = kBKE / kMmaK;  // = 4
-    static constexpr int kTmemCols = 2 * BN;         // double-buffered accumulator
-    static constexpr int kStageOut = 2 * 32 * OutTraits<OUT>::kRowBytes;  // per epilogue warp: 2 buffers
-    static constexpr int kSmemBytes = STAGES * (kAStage + kBStage) + 4 * kStageOut + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kMmaPerSub = kBKE / kMmaK;  // = 4
+    static constexpr int kMmaPerStage = kMmaPerSub;  // (per k-subtile and m-tile)
+    static constexpr int kTmemCols = 2 * MT * BN;    // double-buffered accumulators
+    // epilogue: two 128-row x 128-byte staging tiles, one TMA store each
+    static constexpr int kOutCols = (OUT == OUT_BF16 || OUT == OUT_F16) ? 64 : 32;
+    static constexpr int kOutTile = kBM * 128;
+    static constexpr int kStageOut = 2 * 32 * OutTraits<OUT>::kRowBytes;  // (CTA-pair kernel)
+    static constexpr int kSmemBytes =
+        STAGES * (kAStageK + kBStage) + 2 * kOutTile + 1024 /*align*/ + 256 /*barriers*/;
     static_assert(BN % kNC == 0, "BN must be a multiple of the swizzle atom width");
     static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 };
 
-template <int ELEM, int OUT, int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+// Per-stage work is sized so the fixed costs amortise: the MMA issuer's
+// handshake (wait, fence, commit ~250-450 cycles, tools/mma_bench.cu) and the
+// SM's TMA unit (~200+ cycles per operation whatever its size,
+// tools/tma_bench.cu).  MT m-tiles per CTA share every filter load and fetch
+// their pixels with ONE im2col box of MT*128 pixels; KSUB k-subtiles per
+// stage multiply the MMAs per handshake.
+template <int ELEM, int OUT, int BN, int STAGES, int KSUB, int MT>
+__global__ void __launch_bounds__(kThreadsGeneric, 1)
     conv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_y, const ConvParams p) {
-    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES>;
+    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES, KSUB, MT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *smem_a = smem;
-    uint8_t *smem_b = smem + STAGES * kAStage;
+    uint8_t *smem_b = smem + STAGES * Cfg::kAStageK;
     uint8_t *smem_out = smem_b + STAGES * Cfg::kBStage;  // epilogue staging, 1024-aligned
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_out + 4 * Cfg::kStageOut);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_out + 2 * Cfg::kOutTile);
     uint64_t *full = bars;
     uint64_t *empty = bars + STAGES;
     uint64_t *tfull = bars + 2 * STAGES;
@@ -217,14 +266,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    const long long total_tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
+    const long long total_tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;  // m_tiles of kRows pixels
+    const int k_subs = p.k_stages;                       // k-subtiles per block (host value)
+    const int k_stages = (k_subs + KSUB - 1) / KSUB;     // pipeline stages per block
+    // bytes of one A row of one tap inside a subtile (128 for >= 64-channel chunks)
+    const int rb = kRowBytes / p.tps;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
         ptx::prefetch_tmap(&tmap_b);
         ptx::prefetch_tmap(&tmap_y);
         for (int i = 0; i < STAGES; ++i) {
-            ptx::mbar_init(&full[i], 2);  // A producer + B producer
+            ptx::mbar_init(&full[i], 2);  // one A producer + one B producer arm each stage
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -239,12 +292,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0 || warp == 3) {
-        // ============ TMA producers: warp 0 = activations (im2col), warp 3 = filter ============
-        // Two issuing threads so A and B loads leave the SM in parallel; each
-        // arms the stage's `full` barrier with its own byte count.
+    if (warp == 0 || warp == 2 || warp == 3 || warp == 8) {
+        // ============ TMA producers ============
+        // A (activations, im2col): warps 0 / 2 take even / odd stages;
+        // B (filter): warps 3 / 8 take even / odd stages.  A TMA costs its
+        // issuing thread ~450 cycles whatever the box size (tools/tma_bench.cu),
+        // so two issuing threads per operand double the fill rate; each stage's
+        // `full` barrier is armed by exactly one A and one B producer.
         if (lane == 0) {
-            const bool is_a = warp == 0;
+            const bool is_a = warp == 0 || warp == 2;
+            const int par = (warp == 2 || warp == 8) ? 1 : 0;
+            uint32_t it = 0;
             const uint64_t pol = is_a ? ptx::policy_evict_normal() : ptx::policy_evict_last();
             const int pq = p.p * p.q;
             int stage = 0;
@@ -255,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
                 const long long m_tile = tile / p.n_tiles;
                 const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
-                const long long m0 = m_tile * kBM;
+                const long long m0 = m_tile * Cfg::kRows;
                 const int n0 = static_cast<int>(m0 / pq);
                 const int rem = static_cast<int>(m0 - static_cast<long long>(n0) * pq);
                 const int p0 = rem / p.q;
@@ -264,44 +322,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int h0 = p0 * p.sh - p.ph;
                 const int nb0 = n_tile * BN;
                 kw.reset();
-                for (int kb = 0; kb < p.k_stages; ++kb) {
-                    timed_wait_g(&empty[stage], phase ^ 1, w_empty);
-                    ptx::mbar_arrive_expect_tx(&full[stage], is_a ? kAStage : Cfg::kBStage);
-                    if (p.tps == 1) {
-                        const int c0 = kw.chunk * Cfg::kBKE;
-                        if (is_a) {
-                            ptx::tma_load_im2col_4d(smem_a + stage * kAStage, &tmap_a, &full[stage], c0, w0, h0, n0,
-                                                    static_cast<uint16_t>(kw.s * p.dw),
-                                                    static_cast<uint16_t>(kw.r * p.dh), pol);
+                for (int kb = 0; kb < k_stages; ++kb) {
+                    const bool mine = ((it++) & 1u) == static_cast<uint32_t>(par);
+                    const int nsub = min(KSUB, k_subs - kb * KSUB);
+                    if (mine) {
+                        timed_wait_g(&empty[stage], phase ^ 1, w_empty);
+                        ptx::mbar_arrive_expect_tx(&full[stage], nsub * (is_a ? Cfg::kASub : Cfg::kBSub));
+                    }
+                    uint8_t *a_st = smem_a + stage * Cfg::kAStageK;
+                    uint8_t *b_st = smem_b + stage * Cfg::kBStage;
+                    for (int u = 0; u < nsub; ++u) {
+                        int brow;
+                        if (p.tps == 1) {
+                            const int c0 = kw.chunk * Cfg::kBKE;
+                            if (is_a && mine)
+                                ptx::tma_load_im2col_4d(a_st + u * Cfg::kASub, &tmap_a, &full[stage], c0, w0, h0, n0,
+                                                        static_cast<uint16_t>(kw.s * p.dw),
+                                                        static_cast<uint16_t>(kw.r * p.dh), pol);
+                            brow = kw.tap * p.c + c0;
+                            kw.next(p.order, p.r, p.s, p.c_chunks);
                         } else {
-                            const int brow = kw.tap * p.c + c0;
-                            uint8_t *b_dst = smem_b + stage * Cfg::kBStage;
-                            if (p.b_3d) {
-                                ptx::tma_load_3d(b_dst, &tmap_b, &full[stage], 0, brow, nb0 / Cfg::kNC, pol);
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < BN / Cfg::kNC; ++j)
-                                    ptx::tma_load_2d(b_dst + j * (Cfg::kBKE * kRowBytes), &tmap_b, &full[stage],
-                                                     nb0 + j * Cfg::kNC, brow, pol);
+                            // small-C layers: pack tps taps side by side along the
+                            // reduction (the paper's multi-tile packing, §4.2); tap t
+                            // occupies a (kRows x rb) block
+                            const int tap0 = (kb * KSUB + u) * p.tps;
+                            if (is_a && mine) {
+                                for (int t = 0; t < p.tps; ++t) {
+                                    const int tap = min(tap0 + t, p.rs - 1);  // past-the-end taps meet zero filter rows
+                                    const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
+                                    ptx::tma_load_im2col_4d(a_st + u * Cfg::kASub + t * (Cfg::kRows * rb), &tmap_a,
+                                                            &full[stage], 0, w0, h0, n0,
+                                                            static_cast<uint16_t>(s * p.dw),
+                                                            static_cast<uint16_t>(r * p.dh), pol);
+                                }
                             }
+                            brow = tap0 * p.c;
                         }
-                        kw.next(p.order, p.r, p.s, p.c_chunks);
-                    } else {
-                        // small-C layers: pack tps taps side by side along the
-                        // reduction (the paper's multi-tile packing, §4.2)
-                        const int tap0 = kb * p.tps;
-                        if (is_a) {
-                            const int blk = kAStage / p.tps;
-                            for (int t = 0; t < p.tps; ++t) {
-                                const int tap = min(tap0 + t, p.rs - 1);  // past-the-end taps meet zero filter rows
-                                const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
-                                ptx::tma_load_im2col_4d(smem_a + stage * kAStage + t * blk, &tmap_a, &full[stage], 0,
-                                                        w0, h0, n0, static_cast<uint16_t>(s * p.dw),
-                                                        static_cast<uint16_t>(r * p.dh), pol);
-                            }
-                        } else {
-                            const int brow = tap0 * p.c;
-                            uint8_t *b_dst = smem_b + stage * Cfg::kBStage;
+                        if (!is_a && mine) {
+                            uint8_t *b_dst = b_st + u * Cfg::kBSub;
                             if (p.b_3d) {
                                 ptx::tma_load_3d(b_dst, &tmap_b, &full[stage], 0, brow, nb0 / Cfg::kNC, pol);
                             } else {
@@ -318,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (IMCONV_INSTRUMENT && p.dbg && is_a) {
+            if (IMCONV_INSTRUMENT && p.dbg && warp == 0) {
                 p.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
                 p.dbg[blockIdx.x * 8 + 1] = w_empty;
             }
@@ -327,27 +385,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ===================== tcgen05 MMA issuer =====================
         const uint32_t idesc = make_idesc<ELEM, BN>();
+        // A layout of one (tap, m-tile) operand: 128 rows x rb bytes; tap blocks
+        // of kRows rows; m-tile mt starts mt*128 rows into its tap block
         uint32_t a_lbo, a_sbo, a_layout;
         switch (p.a_layout) {
             case A_SW128: a_lbo = 16; a_sbo = 1024; a_layout = ptx::LAYOUT_SW128; break;
             case A_SW64: a_lbo = 16; a_sbo = 512; a_layout = ptx::LAYOUT_SW64; break;
             case A_SW32: a_lbo = 16; a_sbo = 256; a_layout = ptx::LAYOUT_SW32; break;
-            default: a_lbo = kBM * 16; a_sbo = 128; a_layout = ptx::LAYOUT_NONE; break;
+            default: a_lbo = Cfg::kRows * 16; a_sbo = 128; a_layout = ptx::LAYOUT_NONE; break;
         }
         // descriptors built once; per MMA only the 14-bit start-address field
-        // moves (stage and k-step offsets >> 4 are added to the low word)
-        uint32_t a_kk[Cfg::kMmaPerStage];
+        // moves (stage, subtile, m-tile and k-step offsets >> 4)
+        uint32_t a_kk[Cfg::kMmaPerSub];
 #pragma unroll
-        for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk) {
+        for (int kk = 0; kk < Cfg::kMmaPerSub; ++kk) {
             uint32_t off;
             switch (p.a_layout) {
                 case A_SW128: off = kk * 32; break;
-                case A_SW64: off = (kk >> 1) * (kBM * 64) + (kk & 1) * 32; break;
-                case A_SW32: off = kk * (kBM * 32); break;
-                default: off = kk * 2 * (kBM * 16); break;
+                case A_SW64: off = (kk >> 1) * (Cfg::kRows * 64) + (kk & 1) * 32; break;
+                case A_SW32: off = kk * (Cfg::kRows * 32); break;
+                default: off = kk * 2 * (Cfg::kRows * 16); break;
             }
             a_kk[kk] = off >> 4;
         }
+        const uint32_t a_mt = static_cast<uint32_t>((kBM * rb) >> 4);  // m-tile step inside a tap block
         const uint64_t adesc0 = ptx::smem_desc(ptx::smem_u32(smem_a), a_lbo, a_sbo, a_layout);
         const uint64_t bdesc0 =
             ptx::smem_desc(ptx::smem_u32(smem_b), Cfg::kBKE * kRowBytes, 1024, ptx::LAYOUT_SW128);
@@ -360,22 +421,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             timed_wait_g(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
-            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-            for (int kb = 0; kb < p.k_stages; ++kb) {
+            const uint32_t d_base = tmem_base + static_cast<uint32_t>(acc * MT * BN);
+            for (int kb = 0; kb < k_stages; ++kb) {
                 timed_wait_g(&full[stage], phase, w_full);
                 ptx::tc_fence_after();
                 if (lane == 0) {
-                    const uint64_t a_st = adesc0 + static_cast<uint64_t>((stage * kAStage) >> 4);
+                    const int nsub = min(KSUB, k_subs - kb * KSUB);
+                    const uint64_t a_st = adesc0 + static_cast<uint64_t>((stage * Cfg::kAStageK) >> 4);
                     const uint64_t b_st = bdesc0 + static_cast<uint64_t>((stage * Cfg::kBStage) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk) {
-                        const uint64_t adesc = a_st + a_kk[kk];
-                        const uint64_t bdesc = b_st + static_cast<uint64_t>((kk * Cfg::kMmaK * kRowBytes) >> 4);
-                        const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
-                        if constexpr (ELEM == ELEM_I8)
-                            ptx::mma_i8(d_tmem, adesc, bdesc, idesc, accum);
-                        else
-                            ptx::mma_f16(d_tmem, adesc, bdesc, idesc, accum);
+                    for (int u = 0; u < KSUB; ++u) {
+                        if (u < nsub) {
+#pragma unroll
+                            for (int kk = 0; kk < Cfg::kMmaPerSub; ++kk) {
+                                const uint64_t bdesc =
+                                    b_st + static_cast<uint64_t>((u * Cfg::kBSub + kk * Cfg::kMmaK * kRowBytes) >> 4);
+                                const uint32_t accum = (kb | u | kk) != 0 ? 1u : 0u;
+#pragma unroll
+                                for (int mt = 0; mt < MT; ++mt) {
+                                    const uint64_t adesc =
+                                        a_st + static_cast<uint64_t>((u * Cfg::kASub) >> 4) + mt * a_mt + a_kk[kk];
+                                    if constexpr (ELEM == ELEM_I8)
+                                        ptx::mma_i8(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                    else
+                                        ptx::mma_f16(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                }
+                            }
+                        }
                     }
                     ptx::mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
                 }
@@ -385,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     phase ^= 1;
                 }
             }
-            if (lane == 0) ptx::mma_commit(&tfull[acc]);  // accumulator complete -> epilogue
+            if (lane == 0) ptx::mma_commit(&tfull[acc]);  // accumulators complete -> epilogue
             __syncwarp();
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
@@ -395,11 +467,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.dbg[blockIdx.x * 8 + 3] = w_tempty;
             p.dbg[blockIdx.x * 8 + 4] = w_full;
         }
-    } else if (warp >= 4) {
-        // ============ epilogue: TMEM -> registers -> swizzled smem -> TMA store ============
+    } else if (warp >= 4 && warp < 8) {
+        // ===== epilogue: TMEM -> registers -> one swizzled 128-row tile -> ONE TMA store =====
+        // The SM's TMA unit costs ~200+ cycles per operation whatever its size
+        // (tools/tma_bench.cu), so the four epilogue warps stage a whole
+        // 128 x 128-byte tile and a single thread stores it.
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32) = block rows
-        uint8_t *stage_buf = smem_out + quarter * Cfg::kStageOut;
-        constexpr int kBuf = 32 * OutTraits<OUT>::kRowBytes;
+        const uint32_t row = quarter * 32 + lane;
+        const bool issuer = (warp == 4 && lane == 0);
+        constexpr int kOC = Cfg::kOutCols;
         int acc = 0;
         uint32_t acc_phase = 0;
         uint32_t chunk_ctr = 0;
@@ -408,29 +484,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
-            const int row0 = static_cast<int>(m_tile * kBM) + quarter * 32;
             timed_wait_g(&tfull[acc], acc_phase, w_tfull);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int j = 0; j < BN / 32; ++j) {
-                const int col0 = n_tile * BN + j * 32;
-                uint32_t v[32];
-                const uint32_t taddr =
-                    tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + j * 32);
-                ptx::tmem_ld_32x32b_x32(taddr, v);
-                ptx::tmem_ld_wait();
-                if (col0 >= p.k) continue;  // warp-uniform: whole chunk past the last channel
-                uint8_t *buf = stage_buf + (chunk_ctr & 1) * kBuf;
-                if (lane == 0) ptx::tma_store_wait_read<1>();  // the store issued 2 chunks ago has read buf
-                __syncwarp();
-                stage_row_chunk<OUT>(buf, lane, v);
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::tma_store_2d(&tmap_y, buf, col0, row0);  // rows >= M / cols >= K are clipped
-                    ptx::tma_store_commit();
+            for (int mt = 0; mt < MT; ++mt) {
+                const long long row0 = m_tile * Cfg::kRows + mt * kBM;
+#pragma unroll 1
+                for (int j = 0; j < BN / kOC; ++j) {
+                    const int col0 = n_tile * BN + j * kOC;
+                    uint32_t v[kOC];
+                    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                           static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC);
+#pragma unroll
+                    for (int h = 0; h < kOC / 32; ++h)
+                        ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
+                    ptx::tmem_ld_wait();
+                    if (col0 >= p.k || row0 >= p.m) continue;  // uniform over the 4 warps
+                    uint8_t *buf = smem_out + (chunk_ctr & 1) * Cfg::kOutTile;
+                    if (issuer) ptx::tma_store_wait_read<1>();  // the store issued 2 chunks ago has read buf
+                    ptx::named_bar_sync(1, 128);
+                    stage_row128<OUT>(buf, row, v);
+                    ptx::fence_proxy_async_smem();
+                    ptx::named_bar_sync(1, 128);
+                    if (issuer) {
+                        ptx::tma_store_2d(&tmap_y, buf, col0, static_cast<int>(row0));  // clipped at M / K
+                        ptx::tma_store_commit();
+                    }
+                    ++chunk_ctr;
                 }
-                ++chunk_ctr;
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -438,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if (lane == 0) ptx::tma_store_wait<0>();
+        if (issuer) ptx::tma_store_wait<0>();
         __syncwarp();
         if (IMCONV_INSTRUMENT && p.dbg && lane == 0 && quarter == 0) {
             p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;

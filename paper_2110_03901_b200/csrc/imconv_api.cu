@@ -83,18 +83,18 @@ CUtensorMapDataType tmap_dtype(int in_dtype) {
 
 int elem_bytes(int in_dtype) { return in_dtype == IMCONV_I8 ? 1 : 2; }
 
-template <int ELEM, int OUT, int BN, int STAGES>
+template <int ELEM, int OUT, int BN, int STAGES, int KSUB, int MT>
 int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const ConvParams &p, int grid,
                 cudaStream_t st) {
-    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES>;
-    auto kern = conv_fwd_kernel<ELEM, OUT, BN, STAGES>;
+    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES, KSUB, MT>;
+    auto kern = conv_fwd_kernel<ELEM, OUT, BN, STAGES, KSUB, MT>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid, kThreads, Cfg::kSmemBytes, st>>>(ta, tb, ty, p);
+    kern<<<grid, kThreadsGeneric, Cfg::kSmemBytes, st>>>(ta, tb, ty, p);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
@@ -130,16 +130,33 @@ int dispatch_bn_2sm(int bn, const CUtensorMap &ta, const CUtensorMap &tb, const 
 }
 
 // BN -> pipeline depth that fits ~200 KB of shared memory.
+// Block shape -> pipeline depth that fits the shared memory:
+//   variant 0 (default N <= 128): MT = 2 m-tiles per CTA, 1 k-subtile per stage
+//   variant 1 (IMCONV_FLAG_MT1):  MT = 1, KSUB = 2
+//   variant 2 (IMCONV_FLAG_KSUB1): MT = 1, KSUB = 1
+// N = 256 always runs MT = 1, KSUB = 1 (4 x 128-cycle MMAs per stage).
 template <int ELEM, int OUT>
-int dispatch_bn(int bn, const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const ConvParams &p,
-                int grid, cudaStream_t st) {
+int dispatch_bn(int bn, int variant, const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty,
+                const ConvParams &p, int grid, cudaStream_t st) {
     if constexpr (ELEM == ELEM_I8) {
-        if (bn == 128) return launch_conv<ELEM, OUT, 128, 6>(ta, tb, ty, p, grid, st);
-        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4>(ta, tb, ty, p, grid, st);
+        if (bn == 128) {
+            if (variant == 0) return launch_conv<ELEM, OUT, 128, 4, 1, 2>(ta, tb, ty, p, grid, st);
+            if (variant == 1) return launch_conv<ELEM, OUT, 128, 3, 2, 1>(ta, tb, ty, p, grid, st);
+            return launch_conv<ELEM, OUT, 128, 6, 1, 1>(ta, tb, ty, p, grid, st);
+        }
+        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4, 1, 1>(ta, tb, ty, p, grid, st);
     } else {
-        if (bn == 64) return launch_conv<ELEM, OUT, 64, 8>(ta, tb, ty, p, grid, st);
-        if (bn == 128) return launch_conv<ELEM, OUT, 128, 6>(ta, tb, ty, p, grid, st);
-        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4>(ta, tb, ty, p, grid, st);
+        if (bn == 64) {
+            if (variant == 0) return launch_conv<ELEM, OUT, 64, 4, 1, 2>(ta, tb, ty, p, grid, st);
+            if (variant == 1) return launch_conv<ELEM, OUT, 64, 4, 2, 1>(ta, tb, ty, p, grid, st);
+            return launch_conv<ELEM, OUT, 64, 8, 1, 1>(ta, tb, ty, p, grid, st);
+        }
+        if (bn == 128) {
+            if (variant == 0) return launch_conv<ELEM, OUT, 128, 4, 1, 2>(ta, tb, ty, p, grid, st);
+            if (variant == 1) return launch_conv<ELEM, OUT, 128, 3, 2, 1>(ta, tb, ty, p, grid, st);
+            return launch_conv<ELEM, OUT, 128, 6, 1, 1>(ta, tb, ty, p, grid, st);
+        }
+        if (bn == 256) return launch_conv<ELEM, OUT, 256, 4, 1, 1>(ta, tb, ty, p, grid, st);
     }
     return IMCONV_EINVAL;
 }
@@ -385,6 +402,22 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     const int bn = pick_bn(a->in_dtype, K, a->tile_n);
     if (bn < 0) return IMCONV_EINVAL;
 
+    // ---- block shape: single CTA or CTA pair (cta_group::2, B split across the pair) ----
+    // pairs need whole swizzle-atom columns per CTA (BN >= 128 bf16 / 256 int8)
+    // and enough 256-row blocks to fill the clusters.
+    const int64_t m_tiles_ = (M + kBM - 1) / kBM;
+    const int64_t n_tiles_ = (K + bn - 1) / bn;
+    const long long pair_tiles = ((m_tiles_ + 1) / 2) * n_tiles_;
+    const bool pair_ok = (a->in_dtype == IMCONV_I8) ? bn == 256 : bn >= 128;
+    // Measured (tools/run_layer.py --flags 1/2): once the producers issue one
+    // TMA per operand per stage, single CTAs match or beat pairs on the
+    // ResNet-50 shapes, so pairs are opt-in for now.
+    const bool use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && (a->flags & IMCONV_FLAG_CTA_PAIR) &&
+                          pair_tiles >= 1;
+    // single-CTA block shape (see dispatch_bn): N <= 128 -> 2 m-tiles per CTA
+    const int variant = (a->flags & IMCONV_FLAG_KSUB1) ? 2 : (a->flags & IMCONV_FLAG_MT1) ? 1 : 0;
+    const int mt = (!use_pair && bn <= 128 && variant == 0) ? 2 : 1;
+
     // ---- A operand: im2col tensor map over NHWC ----
     const int64_t cbytes = C * E;
     const int row_bytes = cbytes >= 128 ? 128 : static_cast<int>(cbytes);  // 16, 32, 64 or 128
@@ -411,7 +444,8 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         int upper[2] = {static_cast<int>(up_w), static_cast<int>(up_h)};
         cuuint32_t estride[4] = {1, static_cast<cuuint32_t>(a->stride_w), static_cast<cuuint32_t>(a->stride_h), 1};
         CUresult cr = g_encode_im2col(&ta, tmap_dtype(a->in_dtype), 4, const_cast<void *>(a->x), gdim, gstride,
-                                      lower, upper, static_cast<cuuint32_t>(row_bytes / E), kBM, estride,
+                                      lower, upper, static_cast<cuuint32_t>(row_bytes / E),
+                                      static_cast<cuuint32_t>(kBM * mt), estride,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, a_swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
@@ -420,19 +454,6 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         if (g_driver_version <= 13010 && N * H * W * C * E < 131072)
             reinterpret_cast<uint64_t *>(&ta)[1] &= ~(1ull << 21);
     }
-    // ---- block shape: single CTA or CTA pair (cta_group::2, B split across the pair) ----
-    // pairs need whole swizzle-atom columns per CTA (BN >= 128 bf16 / 256 int8)
-    // and enough 256-row blocks to fill the clusters.
-    const int64_t m_tiles_ = (M + kBM - 1) / kBM;
-    const int64_t n_tiles_ = (K + bn - 1) / bn;
-    const long long pair_tiles = ((m_tiles_ + 1) / 2) * n_tiles_;
-    const bool pair_ok = (a->in_dtype == IMCONV_I8) ? bn == 256 : bn >= 128;
-    // Measured (tools/run_layer.py --flags 1/2): once the producers issue one
-    // TMA per operand per stage, single CTAs match or beat pairs on the
-    // ResNet-50 shapes, so pairs are opt-in for now.
-    const bool use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && (a->flags & IMCONV_FLAG_CTA_PAIR) &&
-                          pair_tiles >= 1;
-
     // ---- B operand: the HWCN filter as (R*S*C rows, K cols).  When K is a whole
     // number of 128-byte column chunks it is viewed 3-D {chunk cols, rows, chunks}
     // so ONE TMA instruction fetches all of a stage's B chunks. ----
@@ -463,7 +484,8 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
     }
 
-    // ---- output: tiled map over y viewed as (M, K), 32x32 store boxes ----
+    // ---- output: tiled map over y viewed as (M, K).  Single-CTA kernel: one
+    // 128-row x 128-byte box per store; CTA pairs: 32 x 32 boxes. ----
     CUtensorMap ty;
     std::memset(&ty, 0, sizeof(ty));
     {
@@ -474,11 +496,12 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
                                                               : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
         cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
         cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * eo)};
-        cuuint32_t box[2] = {32, 32};
+        cuuint32_t box[2] = {use_pair ? 32u : static_cast<cuuint32_t>(128 / eo), use_pair ? 32u : 128u};
         cuuint32_t estride[2] = {1, 1};
+        CUtensorMapSwizzle swz = use_pair ? (eo == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)
+                                          : CU_TENSOR_MAP_SWIZZLE_128B;
         CUresult cr = g_encode_tiled(&ty, dt, 2, a->y, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                     eo == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                     swz, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
     }
 
@@ -499,7 +522,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     p.p = static_cast<int>(P);
     p.q = static_cast<int>(Q);
     p.m = M;
-    p.m_tiles = static_cast<int>((M + kBM - 1) / kBM);
+    p.m_tiles = static_cast<int>((M + kBM * mt - 1) / (kBM * mt));
     p.n_tiles = static_cast<int>((K + bn - 1) / bn);
     p.rs = static_cast<int>(R * S);
     p.tps = tps;
@@ -535,12 +558,12 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     if (grid > tiles) grid = static_cast<int>(tiles);
     switch (a->in_dtype) {
         case IMCONV_BF16:
-            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, grid, st)
-                                              : dispatch_bn<ELEM_BF16, OUT_BF16>(bn, ta, tb, ty, p, grid, st);
+            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
+                                              : dispatch_bn<ELEM_BF16, OUT_BF16>(bn, variant, ta, tb, ty, p, grid, st);
         case IMCONV_F16:
-            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_F16, OUT_F32>(bn, ta, tb, ty, p, grid, st)
-                                              : dispatch_bn<ELEM_F16, OUT_F16>(bn, ta, tb, ty, p, grid, st);
-        case IMCONV_I8: return dispatch_bn<ELEM_I8, OUT_I32>(bn, ta, tb, ty, p, grid, st);
+            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_F16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
+                                              : dispatch_bn<ELEM_F16, OUT_F16>(bn, variant, ta, tb, ty, p, grid, st);
+        case IMCONV_I8: return dispatch_bn<ELEM_I8, OUT_I32>(bn, variant, ta, tb, ty, p, grid, st);
         default: return IMCONV_EDTYPE;
     }
 }

@@ -80,17 +80,20 @@ def test_float_golden_tolerance(golden):
 
 
 @pytest.mark.parametrize("tile_n", [64, 128, 256])
-def test_block_shape_and_grid_invariance(rng, tile_n):
+@pytest.mark.parametrize("flags", [0, 4, 8])  # 0: 2 m-tiles per CTA (N<=128), 4: KSUB=1, 8: MT=1 KSUB=2
+def test_block_shape_and_grid_invariance(rng, tile_n, flags):
     P = _P()
-    x = rng.integers(-4, 5, size=(3, 13, 11, 64)).astype(np.int64)
-    w = rng.integers(-4, 5, size=(3, 3, 64, 200)).astype(np.int64)
     from oracle import oracle as O
-    want = O.conv2d_nhwc_i64(x, w, 1, 2, 1, 1, 2, 1)
-    xb = torch.from_numpy(x).float().cuda().bfloat16()
-    wb = torch.from_numpy(w).float().cuda().bfloat16()
-    for ctas in (0, 1, 5):
-        y = P._kernels.conv2d_nhwc(xb, wb, 1, 2, 1, 1, 2, 1, out_dtype=torch.float32, tile_n=tile_n, num_ctas=ctas)
-        assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), ctas
+    for c in (64, 192):  # 9 / 27 k-subtiles: odd counts leave a half-filled last stage
+        x = rng.integers(-4, 5, size=(3, 13, 11, c)).astype(np.int64)
+        w = rng.integers(-4, 5, size=(3, 3, c, 200)).astype(np.int64)
+        want = O.conv2d_nhwc_i64(x, w, 1, 2, 1, 1, 2, 1)
+        xb = torch.from_numpy(x).float().cuda().bfloat16()
+        wb = torch.from_numpy(w).float().cuda().bfloat16()
+        for ctas in (0, 1, 5):
+            y = P._kernels.conv2d_nhwc(xb, wb, 1, 2, 1, 1, 2, 1, out_dtype=torch.float32, tile_n=tile_n,
+                                       num_ctas=ctas, flags=flags)
+            assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), (c, ctas)
 
 
 @pytest.mark.parametrize("order", ["reuse_aware", "filter_major"])

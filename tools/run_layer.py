@@ -45,15 +45,27 @@ def main():
         w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev) * 0.05).to(torch.bfloat16)
     order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[args.order]
     _lib.lib.imconv_debug_set_flags(args.dbg_flags)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    for i in range(args.reps + 1):
-        if i == 1:
-            ev[0].record()
+    def once():
         if args.explicit:
             low = K.im2col_nhwc(x, sp.h_f, sp.w_f, *sp.conv_args(), True)
             gemm_device(low, w.reshape(-1, sp.c_o))
         else:
             conv_device(x, w, *sp.conv_args(), tile_n=args.tile_n, order=order, flags=args.flags)
+
+    once()
+    torch.cuda.synchronize()
+    # the timed launches are replayed from a CUDA graph so host-side launch
+    # latency (ctypes + tensor-map encoding) cannot starve short kernels
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(args.reps):
+            once()
+    g.replay()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    g.replay()
     ev[1].record()
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / args.reps

@@ -18,25 +18,33 @@ using namespace imconv;
 constexpr int kSlots = 8;
 
 // mode 0: 2-D tiled, mode 1: 4-D im2col, mode 2: 4-D tiled (pixel row)
-__global__ void __launch_bounds__(64, 1) tma_stream(const __grid_constant__ CUtensorMap m, int mode, int loads,
+__global__ void __launch_bounds__(128, 1) tma_stream(const __grid_constant__ CUtensorMap m, int mode, int loads,
                                                     int box_bytes, int c_extent, int w_extent, int h_extent,
                                                     long long *out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t full[kSlots], empty[kSlots];
+    __shared__ uint64_t full_all[2][kSlots], empty_all[2][kSlots];
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kSlots; ++i) {
-            ptx::mbar_init(&full[i], 1);
-            ptx::mbar_init(&empty[i], 1);
-        }
+        for (int i = 0; i < kSlots; ++i)
+            for (int j = 0; j < 2; ++j) {
+                ptx::mbar_init(&full_all[j][i], 1);
+                ptx::mbar_init(&empty_all[j][i], 1);
+            }
         ptx::fence_barrier_init();
     }
     __syncthreads();
     const uint64_t pol = ptx::policy_evict_normal();
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < loads; ++i) {
-            const int s = i % kSlots;
-            ptx::mbar_wait(&empty[s], ((i / kSlots) & 1) ^ 1);
+    const int nprod = loads < 0 ? 2 : 1;
+    if (loads < 0) loads = -loads;
+    const int per = loads / nprod;
+    const int grp = threadIdx.x >> 6;          // producer/consumer group (0 or 1)
+    const int slots = kSlots / nprod;
+    uint64_t *full = full_all[grp], *empty = empty_all[grp];
+    smem += grp * slots * box_bytes;
+    if ((threadIdx.x & 63) == 0 && grp < nprod) {
+        for (int i = 0; i < per; ++i) {
+            const int s = i % slots;
+            ptx::mbar_wait(&empty[s], ((i / slots) & 1) ^ 1);
             ptx::mbar_arrive_expect_tx(&full[s], box_bytes);
             const int k = (blockIdx.x * 7919 + i * 131) & 1023;
             uint8_t *dst = smem + s * box_bytes;
@@ -49,15 +57,15 @@ __global__ void __launch_bounds__(64, 1) tma_stream(const __grid_constant__ CUte
                 ptx::tma_load_4d(dst, &m, &full[s], 0, 0, k % h_extent, k % 8, pol);
             }
         }
-    } else if (threadIdx.x == 32) {
+    } else if ((threadIdx.x & 63) == 32 && grp < nprod) {
         const long long t0 = clock64();
-        for (int i = 0; i < loads; ++i) {
-            const int s = i % kSlots;
-            ptx::mbar_wait(&full[s], (i / kSlots) & 1);
+        for (int i = 0; i < per; ++i) {
+            const int s = i % slots;
+            ptx::mbar_wait(&full[s], (i / slots) & 1);
             ptx::mbar_arrive(&empty[s]);
         }
         const long long t1 = clock64();
-        if (blockIdx.x == 0) out[0] = t1 - t0;
+        if (blockIdx.x == 0 && grp == 0) out[0] = t1 - t0;
     }
 }
 
@@ -77,13 +85,16 @@ int main() {
     const int loads = 20000;
     auto run = [&](const char *name, const CUtensorMap &m, int mode, int box_bytes) {
         cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlots * box_bytes + 1024);
-        tma_stream<<<148, 64, kSlots * box_bytes + 1024>>>(m, mode, loads, box_bytes, N * H * W, W, H, d);
-        tma_stream<<<148, 64, kSlots * box_bytes + 1024>>>(m, mode, loads, box_bytes, N * H * W, W, H, d);
+        for (int np = 1; np <= 2; ++np) {
+        const int ld = np == 1 ? loads : -loads;
+        tma_stream<<<148, 128, kSlots * box_bytes + 1024>>>(m, mode, ld, box_bytes, N * H * W, W, H, d);
+        tma_stream<<<148, 128, kSlots * box_bytes + 1024>>>(m, mode, ld, box_bytes, N * H * W, W, H, d);
         cudaError_t e = cudaDeviceSynchronize();
         long long c = 0;
         cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
-        printf("%-40s box %6d B: %6.1f cyc/load  %6.1f B/cyc/SM  (%s)\n", name, box_bytes, double(c) / loads,
-               double(box_bytes) * loads / c, cudaGetErrorString(e));
+        printf("%-40s box %6d B, %d producer(s): %6.1f cyc/load  %6.1f B/cyc/SM  (%s)\n", name, box_bytes, np,
+               double(c) / loads, double(box_bytes) * loads / c, cudaGetErrorString(e));
+        }
     };
     {  // 2-D tiled: rows of 128 B (64 bf16), box 64 x R rows
         for (int rows : {32, 64, 128, 256}) {
