@@ -318,19 +318,25 @@ def main(argv=None):
     total_flops = sum(l.spec.flops for l in layers_full)  # all ranks together
     value = total_flops / (ms / 1e3) / 1e12
 
-    # ---- per-layer kernel times (separate pass, events around each launch) ----
+    # ---- per-layer kernel times (separate pass): each layer's `reps` launches
+    # are replayed from their own CUDA graph, so host launch latency cannot
+    # starve short kernels ----
     per_layer = []
     reps = 5
+    side = torch.cuda.Stream()
     for layer, sp, x, w, y in work:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(reps):
+                conv_device(x, w, *sp.conv_args(), y=y)
+        g.replay()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        conv_device(x, w, *sp.conv_args(), y=y)
         evs[0].record()
-        for _ in range(reps):
-            conv_device(x, w, *sp.conv_args(), y=y)
+        g.replay()
         evs[1].record()
         torch.cuda.synchronize()
-        t_ms = evs[0].elapsed_time(evs[1]) / reps
-        per_layer.append((layer, sp, t_ms))
+        per_layer.append((layer, sp, evs[0].elapsed_time(evs[1]) / reps))
+        del g
     kern_ms = sum(t for *_, t in per_layer)
     dtype_peak = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
     hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])

@@ -56,6 +56,8 @@ extern "C" {
 #define IMCONV_FLAG_CTA_PAIR 2    /* use CTA pairs whenever the shape allows   */
 #define IMCONV_FLAG_KSUB1 4       /* one k-subtile per pipeline stage (N<=128 default is 2) */
 #define IMCONV_FLAG_MT1 8         /* one 128-pixel m-tile per CTA (N<=128 default is two)  */
+#define IMCONV_FLAG_GATHER16 16   /* 16-byte pixels: generic kernel with cp.async tap gathers
+                                     instead of the row-band (stride-phase plane) kernel     */
 
 /*
  * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,

@@ -65,6 +65,8 @@ struct ConvParams {
     long long ldy;       // = k
     long long *dbg;      // optional per-CTA role / wait-cycle counters (instrumentation), else nullptr
     int b_3d;            // 1: the filter map is 3-D {chunk cols, rows, chunks}: one TMA per stage for all of B
+    int a_gather;        // 1: 16-byte pixels -- A tap blocks gathered by cp.async warps instead of TMA
+    const uint8_t *x;    // NHWC input (gather mode)
 };
 
 // Division-free walk over the k-subtiles (filter tap <r,s>, channel chunk) of
@@ -132,7 +134,7 @@ struct ElemTraits<ELEM_I8> {
 
 // tcgen05 instruction descriptor: A K-major, B MN-major (HWCN filter rows
 // are contiguous over the output channel), M = 128, N = BN.
-template <int ELEM, int BN>
+template <int ELEM, int BN, int M = kBM>
 __device__ __forceinline__ uint32_t make_idesc() {
     uint32_t d = 0;
     d |= (ELEM == ELEM_I8 ? 2u : 1u) << 4;          // D format: S32 / F32
@@ -141,7 +143,7 @@ __device__ __forceinline__ uint32_t make_idesc() {
     d |= 0u << 15;                                  // A major: K
     d |= 1u << 16;                                  // B major: MN
     d |= static_cast<uint32_t>(BN >> 3) << 17;      // N
-    d |= static_cast<uint32_t>(kBM >> 4) << 24;     // M
+    d |= static_cast<uint32_t>(M >> 4) << 24;       // M (256: CTA pair, cta_group::2)
     return d;
 }
 
@@ -216,14 +218,14 @@ __device__ __forceinline__ void stage_row128(uint8_t *tile, uint32_t row, const 
     }
 }
 
-template <int ELEM, int OUT, int BN, int STAGES, int KSUB = 1, int MT = 1>
+template <int ELEM, int OUT, int BN, int STAGES, int KSUB = 1, int MT = 1, int CG = 1>
 struct ConvCfg {
     static constexpr int kE = ElemTraits<ELEM>::kBytes;
     static constexpr int kBKE = kRowBytes / kE;      // reduction elements per k-subtile
     static constexpr int kNC = kRowBytes / kE;       // n-chunk of one MN-major SW128 atom column
     static constexpr int kRows = MT * kBM;           // output pixels per CTA block (MT accumulators)
     static constexpr int kASub = MT * kAStage;       // bytes of A per k-subtile (one im2col box of kRows pixels)
-    static constexpr int kBSub = BN * kRowBytes;     // bytes of B per k-subtile
+    static constexpr int kBSub = (BN / CG) * kRowBytes;  // bytes of B per k-subtile (per CTA of a pair)
     static constexpr int kAStageK = KSUB * kASub;    // a pipeline stage carries KSUB k-subtiles
     static constexpr int kBStage = KSUB * kBSub;
     static constexpr int kMmaK = 32 / kE;            // reduction elements per tcgen05.mma
@@ -236,7 +238,8 @@ struct ConvCfg {
     static constexpr int kStageOut = 2 * 32 * OutTraits<OUT>::kRowBytes;  // (CTA-pair kernel)
     static constexpr int kSmemBytes =
         STAGES * (kAStageK + kBStage) + 2 * kOutTile + 1024 /*align*/ + 256 /*barriers*/;
-    static_assert(BN % kNC == 0, "BN must be a multiple of the swizzle atom width");
+    static_assert((BN / CG) % kNC == 0, "each CTA must hold whole swizzle-atom columns of B");
+    static_assert(CG == 1 || (MT == 1 && KSUB == 1), "CTA pairs run one m-tile and one k-subtile per stage");
     static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
     static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 };
@@ -247,11 +250,19 @@ struct ConvCfg {
 // tools/tma_bench.cu).  MT m-tiles per CTA share every filter load and fetch
 // their pixels with ONE im2col box of MT*128 pixels; KSUB k-subtiles per
 // stage multiply the MMAs per handshake.
-template <int ELEM, int OUT, int BN, int STAGES, int KSUB, int MT>
+//
+// CG = 2 runs the block on a CTA pair (tcgen05 cta_group::2, launched as a
+// 2-CTA cluster): CTA r gathers pixels [m0 + 128 r, +128) and HALF of the
+// filter tile; the leader issues 256 x BN MMAs reading both CTAs' smem and
+// accumulating 128 rows into each CTA's TMEM.  Both CTAs' TMA loads signal
+// the leader's `full` barrier (armed with both CTAs' bytes); the leader's
+// commits multicast to both CTAs' `empty` / `tfull`; every epilogue warp
+// of both CTAs arrives on the leader's `tempty`.
+template <int ELEM, int OUT, int BN, int STAGES, int KSUB, int MT, int CG>
 __global__ void __launch_bounds__(kThreadsGeneric, 1)
     conv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_y, const ConvParams p) {
-    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES, KSUB, MT>;
+    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES, KSUB, MT, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *smem_a = smem;
@@ -266,7 +277,10 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    const long long total_tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;  // m_tiles of kRows pixels
+    const long long total_tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;  // m_tiles of CG*kRows pixels
+    const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;  // 0 = leader (issues the MMAs)
+    const long long tile_start = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
+    const long long tile_step = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
     const int k_subs = p.k_stages;                       // k-subtiles per block (host value)
     const int k_stages = (k_subs + KSUB - 1) / KSUB;     // pipeline stages per block
     // bytes of one A row of one tap inside a subtile (128 for >= 64-channel chunks)
@@ -277,22 +291,105 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         ptx::prefetch_tmap(&tmap_b);
         ptx::prefetch_tmap(&tmap_y);
         for (int i = 0; i < STAGES; ++i) {
-            ptx::mbar_init(&full[i], 2);  // one A producer + one B producer arm each stage
+            // one A producer + one B producer arm each stage; in gather mode
+            // every lane of the A warp arrives once its copies have landed
+            ptx::mbar_init(&full[i], p.a_gather ? 33 : 2);
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 4);  // one arrival per epilogue warp
+            ptx::mbar_init(&tempty[i], 4 * CG);  // one arrival per epilogue warp (of both CTAs)
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    if (warp == 2) {
+        if constexpr (CG == 2)
+            ptx::tmem_alloc_2sm<Cfg::kTmemCols>(tmem_slot);
+        else
+            ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2)
+        ptx::cluster_sync();
+    else
+        __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0 || warp == 2 || warp == 3 || warp == 8) {
+    if (CG == 1 && STAGES >= 4 && p.a_gather && (warp == 0 || warp == 2)) {  // (>= 2 ring slots per gather warp)
+        // ===== A producers for 16-byte pixels (bf16 C = 8: the ResNet stem) =====
+        // A 16-byte TMA element costs as much TMA time as a 128-byte one, so the
+        // tap blocks (kRows rows x 16 B, no-swizzle K-major core matrices, 8 taps
+        // per stage) are gathered by all 32 lanes with cp.async; out-of-image
+        // taps are zero-filled (src-size 0).  Warp 0 / 2 take even / odd stages.
+        // Completion: wait_group (lagged) -> proxy fence -> per-lane arrive.
+        constexpr int kRowsPerLane = Cfg::kRows / 32;
+        const int par = warp == 2 ? 1 : 0;
+        const int pq = p.p * p.q;
+        const size_t img = static_cast<size_t>(p.h) * p.w;
+        const uint32_t a0 = ptx::smem_u32(smem_a);
+        // completions are retired one stage late: each warp owns only STAGES/2
+        // ring slots, so a longer lag would wait on its own un-arrived stage
+        constexpr int kLag = 1;
+        int pend[kLag + 1];
+        int npend = 0;
+        uint32_t it = 0;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
+            const long long m_tile = tile / p.n_tiles;
+            const long long m0 = m_tile * Cfg::kRows;
+            // this lane's rows: lane + 32 i
+            int hb[kRowsPerLane], wb[kRowsPerLane];
+            const uint8_t *base[kRowsPerLane];
+#pragma unroll
+            for (int i = 0; i < kRowsPerLane; ++i) {
+                const long long m = m0 + lane + 32 * i;
+                const bool ok = m < p.m;
+                const int n = ok ? static_cast<int>(m / pq) : 0;
+                const int rem = ok ? static_cast<int>(m - static_cast<long long>(n) * pq) : 0;
+                const int op = rem / p.q, oq = rem - (rem / p.q) * p.q;
+                hb[i] = ok ? op * p.sh - p.ph : -(1 << 20);  // never in range when past M
+                wb[i] = oq * p.sw - p.pw;
+                base[i] = p.x + static_cast<size_t>(n) * img * 16;
+            }
+            for (int kb = 0; kb < k_stages; ++kb) {
+                const bool mine = ((it++) & 1u) == static_cast<uint32_t>(par);
+                if (mine) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t dst0 = a0 + stage * Cfg::kAStageK;
+                    for (int t = 0; t < p.tps; ++t) {
+                        const int tap = min(kb * p.tps + t, p.rs - 1);  // past-the-end taps meet zero filter rows
+                        const int r = tap / p.s, sx = tap - (tap / p.s) * p.s;
+                        const uint32_t dblk = dst0 + t * (Cfg::kRows * 16);
+#pragma unroll
+                        for (int i = 0; i < kRowsPerLane; ++i) {
+                            const int hh = hb[i] + r * p.dh, ww = wb[i] + sx * p.dw;
+                            const bool ok = hh >= 0 && hh < p.h && ww >= 0 && ww < p.w;
+                            const uint8_t *src = ok ? base[i] + (static_cast<size_t>(hh) * p.w + ww) * 16 : p.x;
+                            ptx::cp_async_16(dblk + (lane + 32 * i) * 16, src, ok ? 16u : 0u);
+                        }
+                    }
+                    ptx::cp_async_commit();
+                    pend[npend++] = stage;
+                    if (npend > kLag) {
+                        ptx::cp_async_wait<kLag>();
+                        ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05
+                        ptx::mbar_arrive(&full[pend[0]]);
+                        for (int u = 0; u < kLag; ++u) pend[u] = pend[u + 1];
+                        --npend;
+                    }
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        ptx::cp_async_wait<0>();
+        ptx::fence_proxy_async_smem();
+        for (int u = 0; u < npend; ++u) ptx::mbar_arrive(&full[pend[u]]);
+    } else if (warp == 0 || warp == 2 || warp == 3 || warp == 8) {
         // ============ TMA producers ============
         // A (activations, im2col): warps 0 / 2 take even / odd stages;
         // B (filter): warps 3 / 8 take even / odd stages.  A TMA costs its
@@ -310,24 +407,28 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             long long w_empty = 0;
             const long long t_start = clock64();
             KWalk kw;
-            for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+            for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
                 const long long m_tile = tile / p.n_tiles;
                 const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
-                const long long m0 = m_tile * Cfg::kRows;
+                const long long m0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows;
                 const int n0 = static_cast<int>(m0 / pq);
                 const int rem = static_cast<int>(m0 - static_cast<long long>(n0) * pq);
                 const int p0 = rem / p.q;
                 const int q0 = rem - p0 * p.q;
                 const int w0 = q0 * p.sw - p.pw;  // base pixel (im2col bounding-box coordinates)
                 const int h0 = p0 * p.sh - p.ph;
-                const int nb0 = n_tile * BN;
+                const int nb0 = n_tile * BN + static_cast<int>(rank) * (BN / CG);
                 kw.reset();
                 for (int kb = 0; kb < k_stages; ++kb) {
                     const bool mine = ((it++) & 1u) == static_cast<uint32_t>(par);
                     const int nsub = min(KSUB, k_subs - kb * KSUB);
+                    // completion barrier: own `full` (single CTA) or the leader's (pair)
+                    const uint32_t fb = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[stage]), 0)
+                                                : ptx::smem_u32(&full[stage]);
                     if (mine) {
                         timed_wait_g(&empty[stage], phase ^ 1, w_empty);
-                        ptx::mbar_arrive_expect_tx(&full[stage], nsub * (is_a ? Cfg::kASub : Cfg::kBSub));
+                        if (rank == 0)
+                            ptx::mbar_arrive_expect_tx(&full[stage], CG * nsub * (is_a ? Cfg::kASub : Cfg::kBSub));
                     }
                     uint8_t *a_st = smem_a + stage * Cfg::kAStageK;
                     uint8_t *b_st = smem_b + stage * Cfg::kBStage;
@@ -335,10 +436,16 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         int brow;
                         if (p.tps == 1) {
                             const int c0 = kw.chunk * Cfg::kBKE;
-                            if (is_a && mine)
-                                ptx::tma_load_im2col_4d(a_st + u * Cfg::kASub, &tmap_a, &full[stage], c0, w0, h0, n0,
-                                                        static_cast<uint16_t>(kw.s * p.dw),
-                                                        static_cast<uint16_t>(kw.r * p.dh), pol);
+                            if (is_a && mine) {
+                                if constexpr (CG == 2)
+                                    ptx::tma_load_im2col_4d_2sm(a_st + u * Cfg::kASub, &tmap_a, fb, c0, w0, h0, n0,
+                                                                static_cast<uint16_t>(kw.s * p.dw),
+                                                                static_cast<uint16_t>(kw.r * p.dh), pol);
+                                else
+                                    ptx::tma_load_im2col_4d(a_st + u * Cfg::kASub, &tmap_a, &full[stage], c0, w0, h0,
+                                                            n0, static_cast<uint16_t>(kw.s * p.dw),
+                                                            static_cast<uint16_t>(kw.r * p.dh), pol);
+                            }
                             brow = kw.tap * p.c + c0;
                             kw.next(p.order, p.r, p.s, p.c_chunks);
                         } else {
@@ -350,17 +457,32 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                                 for (int t = 0; t < p.tps; ++t) {
                                     const int tap = min(tap0 + t, p.rs - 1);  // past-the-end taps meet zero filter rows
                                     const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
-                                    ptx::tma_load_im2col_4d(a_st + u * Cfg::kASub + t * (Cfg::kRows * rb), &tmap_a,
-                                                            &full[stage], 0, w0, h0, n0,
-                                                            static_cast<uint16_t>(s * p.dw),
-                                                            static_cast<uint16_t>(r * p.dh), pol);
+                                    if constexpr (CG == 2)
+                                        ptx::tma_load_im2col_4d_2sm(a_st + u * Cfg::kASub + t * (Cfg::kRows * rb),
+                                                                    &tmap_a, fb, 0, w0, h0, n0,
+                                                                    static_cast<uint16_t>(s * p.dw),
+                                                                    static_cast<uint16_t>(r * p.dh), pol);
+                                    else
+                                        ptx::tma_load_im2col_4d(a_st + u * Cfg::kASub + t * (Cfg::kRows * rb), &tmap_a,
+                                                                &full[stage], 0, w0, h0, n0,
+                                                                static_cast<uint16_t>(s * p.dw),
+                                                                static_cast<uint16_t>(r * p.dh), pol);
                                 }
                             }
                             brow = tap0 * p.c;
                         }
                         if (!is_a && mine) {
                             uint8_t *b_dst = b_st + u * Cfg::kBSub;
-                            if (p.b_3d) {
+                            if constexpr (CG == 2) {
+                                if (p.b_3d) {
+                                    ptx::tma_load_3d_2sm(b_dst, &tmap_b, fb, 0, brow, nb0 / Cfg::kNC, pol);
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < (BN / CG) / Cfg::kNC; ++j)
+                                        ptx::tma_load_2d_2sm(b_dst + j * (Cfg::kBKE * kRowBytes), &tmap_b, fb,
+                                                             nb0 + j * Cfg::kNC, brow, pol);
+                                }
+                            } else if (p.b_3d) {
                                 ptx::tma_load_3d(b_dst, &tmap_b, &full[stage], 0, brow, nb0 / Cfg::kNC, pol);
                             } else {
 #pragma unroll
@@ -382,9 +504,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             }
         }
         __syncwarp();
-    } else if (warp == 1) {
-        // ===================== tcgen05 MMA issuer =====================
-        const uint32_t idesc = make_idesc<ELEM, BN>();
+    } else if (warp == 1 && rank == 0) {
+        // ===================== tcgen05 MMA issuer (the leader CTA of a pair) =====================
+        const uint32_t idesc = make_idesc<ELEM, BN, CG * kBM>();
         // A layout of one (tap, m-tile) operand: 128 rows x rb bytes; tap blocks
         // of kRows rows; m-tile mt starts mt*128 rows into its tap block
         uint32_t a_lbo, a_sbo, a_layout;
@@ -418,7 +540,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         uint32_t acc_phase = 0;
         long long w_tempty = 0, w_full = 0;
         const long long t_start = clock64();
-        for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
             timed_wait_g(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
             const uint32_t d_base = tmem_base + static_cast<uint32_t>(acc * MT * BN);
@@ -441,15 +563,25 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                                 for (int mt = 0; mt < MT; ++mt) {
                                     const uint64_t adesc =
                                         a_st + static_cast<uint64_t>((u * Cfg::kASub) >> 4) + mt * a_mt + a_kk[kk];
-                                    if constexpr (ELEM == ELEM_I8)
+                                    if constexpr (CG == 2) {
+                                        if constexpr (ELEM == ELEM_I8)
+                                            ptx::mma_i8_2sm(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                        else
+                                            ptx::mma_f16_2sm(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                    } else if constexpr (ELEM == ELEM_I8) {
                                         ptx::mma_i8(d_base + mt * BN, adesc, bdesc, idesc, accum);
-                                    else
+                                    } else {
                                         ptx::mma_f16(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                    }
                                 }
                             }
                         }
                     }
-                    ptx::mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+                    // frees the smem slot (in both CTAs of a pair) once these MMAs retire
+                    if constexpr (CG == 2)
+                        ptx::mma_commit_2sm(&empty[stage]);
+                    else
+                        ptx::mma_commit(&empty[stage]);
                 }
                 __syncwarp();
                 if (++stage == STAGES) {
@@ -457,7 +589,12 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                     phase ^= 1;
                 }
             }
-            if (lane == 0) ptx::mma_commit(&tfull[acc]);  // accumulators complete -> epilogue
+            if (lane == 0) {  // accumulators complete -> epilogue(s)
+                if constexpr (CG == 2)
+                    ptx::mma_commit_2sm(&tfull[acc]);
+                else
+                    ptx::mma_commit(&tfull[acc]);
+            }
             __syncwarp();
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
@@ -481,14 +618,14 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         uint32_t chunk_ctr = 0;
         long long w_tfull = 0;
         const long long t_start = clock64();
-        for (long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
             timed_wait_g(&tfull[acc], acc_phase, w_tfull);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int mt = 0; mt < MT; ++mt) {
-                const long long row0 = m_tile * Cfg::kRows + mt * kBM;
+                const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;
 #pragma unroll 1
                 for (int j = 0; j < BN / kOC; ++j) {
                     const int col0 = n_tile * BN + j * kOC;
@@ -515,7 +652,12 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (CG == 2)
+                    ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+                else
+                    ptx::mbar_arrive(&tempty[acc]);
+            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
@@ -527,10 +669,19 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         }
     }
 
-    __syncthreads();
-    if (warp == 2) {
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    if constexpr (CG == 2) {
+        ptx::tc_fence_before();
+        ptx::cluster_sync();  // neither CTA of the pair releases TMEM / smem while its peer still uses them
+        if (warp == 2) {
+            ptx::tc_fence_after();
+            ptx::tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
+        }
+    } else {
+        __syncthreads();
+        if (warp == 2) {
+            ptx::tc_fence_after();
+            ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+        }
     }
 }
 

@@ -34,6 +34,7 @@ namespace imconv {
 
 constexpr int kMaxPairs = 8;  // S <= 16
 constexpr int kProducers = 64;  // warps 2-3 gather the planes
+constexpr int kMaxEntPerThread = 8;  // sw * needed <= 512 plane pixels per input row
 
 struct RowbandParams {
     int n, h, w, k;
@@ -81,7 +82,7 @@ struct RowbandCfg {
     static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
 };
 
-template <int ELEM, int OUT, int BN, int TP>
+template <int ELEM, int OUT, int BN, int TP, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_rowband_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_y,
                         const RowbandParams p) {
@@ -147,8 +148,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (LSU path: a 16-byte TMA element costs as much TMA time as a 128-byte
         // one, so strided 16-byte pixels are gathered by threads instead)
         const int t = threadIdx.x - 64;
-        const int entries = p.sw * p.needed;
+        const int entries = (IMCONV_INSTRUMENT && (p.dbg_flags & 2)) ? 0 : p.sw * p.needed;
         const uint32_t a0 = ptx::smem_u32(smem_a);
+        // this thread's (plane, pixel) entries, fixed for the whole kernel:
+        // smem offset inside a stage and column offset relative to the block
+        uint32_t e_dst[kMaxEntPerThread];
+        int e_col[kMaxEntPerThread];
+        int n_ent = 0;
+#pragma unroll
+        for (int u = 0; u < kMaxEntPerThread; ++u) {
+            const int k = t + u * kProducers;
+            const int e = k / p.needed, j = k - (k / p.needed) * p.needed;
+            e_dst[u] = static_cast<uint32_t>(e * p.plane_bytes + j * 16);
+            e_col[u] = p.sw * j + e;
+            n_ent += k < entries ? 1 : 0;
+        }
         const size_t row_bytes = static_cast<size_t>(p.w) * 16;
         constexpr int kLag = 4;  // cp.async groups kept in flight per thread
         int pend[kLag + 1];
@@ -170,12 +184,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool row_ok = h >= 0 && h < p.h;
                 const uint8_t *xrow = p.x + (static_cast<size_t>(n) * p.h + (row_ok ? h : 0)) * row_bytes;
                 const uint32_t dst0 = a0 + stage * p.a_stage_bytes;
-                for (int k = t; k < ((IMCONV_INSTRUMENT && (p.dbg_flags & 2)) ? 0 : entries); k += kProducers) {
-                    const int e = k / p.needed;
-                    const int j = k - e * p.needed;
-                    const int col = col0 + p.sw * j + e;
-                    const bool ok = row_ok && col >= 0 && col < p.w;
-                    ptx::cp_async_16(dst0 + e * p.plane_bytes + j * 16, xrow + (ok ? col : 0) * 16, ok ? 16u : 0u);
+#pragma unroll
+                for (int u = 0; u < kMaxEntPerThread; ++u) {
+                    if (u < n_ent) {
+                        const int col = col0 + e_col[u];
+                        const bool ok = row_ok && col >= 0 && col < p.w;
+                        ptx::cp_async_16(dst0 + e_dst[u], xrow + (ok ? col : 0) * 16, ok ? 16u : 0u);
+                    }
                 }
                 ptx::cp_async_commit();
                 pend[npend++] = stage;
@@ -218,6 +233,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(smem_b), p.b_chunk_bytes, 1024, ptx::LAYOUT_SW128);
         const int npairs = (IMCONV_INSTRUMENT && (p.dbg_flags & 4)) ? 1 : p.npairs;
+        // register-resident pair descriptors (NP >= npairs, compile-time bound):
+        // the MMA asm statements clobber memory, so table reads from smem would
+        // otherwise be re-issued (and waited on) before every MMA
+        uint64_t adesc_r[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) adesc_r[k] = adesc_tab[k < npairs ? k : 0];
         const uint32_t stage_enc = static_cast<uint32_t>(p.a_stage_bytes >> 4);
         ptx::mbar_wait(bfull, 0);
         int stage = 0;
@@ -235,15 +256,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 {
                     const uint64_t a_add = static_cast<uint64_t>(stage * stage_enc);
+                    int rrs[TP];
+#pragma unroll
+                    for (int j = 0; j < TP; ++j) rrs[j] = rr_tab[i * TP + j];
 #pragma unroll
                     for (int j = 0; j < TP; ++j) {
-                        const int rr = rr_tab[i * TP + j];
+                        const int rr = rrs[j];
                         if (rr < 0) continue;  // warp-uniform
                         const uint64_t b_row = bdesc0 + static_cast<uint64_t>(rr * npairs * 128);
-                        for (int pr = 0; pr < npairs; ++pr)
-                            ptx::mma_f16_elect(d_base + j * BN, adesc_tab[pr] + a_add,
-                                               b_row + static_cast<uint64_t>(pr * 128), idesc,
-                                               (rr | pr) != 0 ? 1u : 0u);
+#pragma unroll
+                        for (int pr = 0; pr < NP; ++pr) {
+                            if (pr < npairs)
+                                ptx::mma_f16_elect(d_base + j * BN, adesc_r[pr] + a_add,
+                                                   b_row + static_cast<uint64_t>(pr * 128), idesc,
+                                                   (rr | pr) != 0 ? 1u : 0u);
+                        }
                     }
                     ptx::mma_commit_elect(&empty[stage]);
                 }

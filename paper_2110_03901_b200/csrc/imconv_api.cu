@@ -18,7 +18,6 @@
 #include "../../include/imconv.h"
 #include "aux_kernels.cuh"
 #include "conv_kernel.cuh"
-#include "conv_kernel_2sm.cuh"
 #include "conv_rowband.cuh"
 
 namespace imconv {
@@ -83,53 +82,55 @@ CUtensorMapDataType tmap_dtype(int in_dtype) {
 
 int elem_bytes(int in_dtype) { return in_dtype == IMCONV_I8 ? 1 : 2; }
 
-template <int ELEM, int OUT, int BN, int STAGES, int KSUB, int MT>
+template <int ELEM, int OUT, int BN, int STAGES, int KSUB, int MT, int CG = 1>
 int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const ConvParams &p, int grid,
                 cudaStream_t st) {
-    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES, KSUB, MT>;
-    auto kern = conv_fwd_kernel<ELEM, OUT, BN, STAGES, KSUB, MT>;
+    using Cfg = ConvCfg<ELEM, OUT, BN, STAGES, KSUB, MT, CG>;
+    auto kern = conv_fwd_kernel<ELEM, OUT, BN, STAGES, KSUB, MT, CG>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+        if (attr_err == cudaSuccess && CG == 2)
+            attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid, kThreadsGeneric, Cfg::kSmemBytes, st>>>(ta, tb, ty, p);
-    ++g_launches;
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : static_cast<int>(e);
-}
-
-template <int ELEM, int OUT, int BN, int STAGES>
-int launch_conv_2sm(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const ConvParams &p,
-                    int grid, cudaStream_t st) {
-    using Cfg = Conv2smCfg<ELEM, OUT, BN, STAGES>;
-    auto kern = conv_fwd_2sm_kernel<ELEM, OUT, BN, STAGES>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    });
-    if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid & ~1, kThreads, Cfg::kSmemBytes, st>>>(ta, tb, ty, p);
-    ++g_launches;
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : static_cast<int>(e);
-}
-
-template <int ELEM, int OUT>
-int dispatch_bn_2sm(int bn, const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty,
-                    const ConvParams &p, int grid, cudaStream_t st) {
-    if constexpr (ELEM == ELEM_I8) {
-        if (bn == 256) return launch_conv_2sm<ELEM, OUT, 256, 6>(ta, tb, ty, p, grid, st);
+    if constexpr (CG == 1) {
+        kern<<<grid, kThreadsGeneric, Cfg::kSmemBytes, st>>>(ta, tb, ty, p);
     } else {
-        if (bn == 128) return launch_conv_2sm<ELEM, OUT, 128, 8>(ta, tb, ty, p, grid, st);
-        if (bn == 256) return launch_conv_2sm<ELEM, OUT, 256, 6>(ta, tb, ty, p, grid, st);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
+        cfg.blockDim = dim3(kThreadsGeneric);
+        cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta, tb, ty, p);
+        if (le != cudaSuccess) return static_cast<int>(le);
+    }
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+// CTA pairs (cta_group::2): one m-tile, one k-subtile per stage, half of B per CTA.
+template <int ELEM, int OUT>
+int dispatch_bn_pair(int bn, const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty,
+                     const ConvParams &p, int grid, cudaStream_t st) {
+    if constexpr (ELEM == ELEM_I8) {
+        if (bn == 256) return launch_conv<ELEM, OUT, 256, 6, 1, 1, 2>(ta, tb, ty, p, grid, st);
+    } else {
+        if (bn == 128) return launch_conv<ELEM, OUT, 128, 8, 1, 1, 2>(ta, tb, ty, p, grid, st);
+        if (bn == 256) return launch_conv<ELEM, OUT, 256, 6, 1, 1, 2>(ta, tb, ty, p, grid, st);
     }
     return IMCONV_EINVAL;
 }
 
-// BN -> pipeline depth that fits ~200 KB of shared memory.
 // Block shape -> pipeline depth that fits the shared memory:
 //   variant 0 (default N <= 128): MT = 2 m-tiles per CTA, 1 k-subtile per stage
 //   variant 1 (IMCONV_FLAG_MT1):  MT = 1, KSUB = 2
@@ -176,10 +177,10 @@ constexpr int kMaxDynSmem = 227 * 1024;
 
 inline int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 
-template <int ELEM, int OUT, int BN, int TP>
+template <int ELEM, int OUT, int BN, int TP, int NP>
 int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandParams &p, int smem, int grid,
                    cudaStream_t st) {
-    auto kern = conv_rowband_kernel<ELEM, OUT, BN, TP>;
+    auto kern = conv_rowband_kernel<ELEM, OUT, BN, TP, NP>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
@@ -261,7 +262,8 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     const int fixed = p.b_bytes + 4 * kStageOut + 1024 /*align*/ + 1024 /*barriers + tables*/;
     const int room = kMaxDynSmem - fixed;
     p.n_stages = std::min(24, room / p.a_stage_bytes);
-    if (p.b_bytes > 128 * 1024 || p.n_stages < 3 || p.in_rows * TP > 256 || 2 * p.n_stages * 8 + 64 > 512)
+    if (p.b_bytes > 128 * 1024 || p.n_stages < 3 || p.in_rows * TP > 256 || 2 * p.n_stages * 8 + 64 > 512 ||
+        p.sw * p.needed > kProducers * kMaxEntPerThread)
         return kNotApplicable;
     const int smem = fixed + p.n_stages * p.a_stage_bytes;
 
@@ -298,11 +300,19 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
     if (grid > p.tiles) grid = static_cast<int>(p.tiles);
     const bool f32 = a->out_dtype == IMCONV_F32;
-#define IMCONV_RB(EL, OUTK)                                                                          \
-    switch (BN) {                                                                                    \
-        case 64: return launch_rowband<EL, OUTK, 64, 4>(tw, ty, p, smem, grid, st);              \
-        case 128: return launch_rowband<EL, OUTK, 128, 2>(tw, ty, p, smem, grid, st);            \
-        default: return launch_rowband<EL, OUTK, 256, 1>(tw, ty, p, smem, grid, st);             \
+#define IMCONV_RB(EL, OUTK)                                                                               \
+    if (p.npairs <= 4) {                                                                                   \
+        switch (BN) {                                                                                      \
+            case 64: return launch_rowband<EL, OUTK, 64, 4, 4>(tw, ty, p, smem, grid, st);                 \
+            case 128: return launch_rowband<EL, OUTK, 128, 2, 4>(tw, ty, p, smem, grid, st);               \
+            default: return launch_rowband<EL, OUTK, 256, 1, 4>(tw, ty, p, smem, grid, st);                \
+        }                                                                                                  \
+    } else {                                                                                               \
+        switch (BN) {                                                                                      \
+            case 64: return launch_rowband<EL, OUTK, 64, 4, 8>(tw, ty, p, smem, grid, st);                 \
+            case 128: return launch_rowband<EL, OUTK, 128, 2, 8>(tw, ty, p, smem, grid, st);               \
+            default: return launch_rowband<EL, OUTK, 256, 1, 8>(tw, ty, p, smem, grid, st);                \
+        }                                                                                                  \
     }
     if (a->in_dtype == IMCONV_BF16) {
         if (f32) { IMCONV_RB(ELEM_BF16, OUT_F32) } else { IMCONV_RB(ELEM_BF16, OUT_BF16) }
@@ -394,7 +404,9 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     rc = sm_count_for_current_device(&sms);
     if (rc) return rc;
 
-    if (a->order != IMCONV_ORDER_FILTER_MAJOR) {
+    // 16-byte pixels: the row-band kernel unless the generic kernel's cp.async
+    // tap gathers are requested (measured 0.47 vs 0.94 ms on the ResNet stem)
+    if (!(a->flags & IMCONV_FLAG_GATHER16) && a->order != IMCONV_ORDER_FILTER_MAJOR) {
         const int rb = try_rowband(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
         if (rb != kNotApplicable) return rb;
     }
@@ -484,8 +496,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
     }
 
-    // ---- output: tiled map over y viewed as (M, K).  Single-CTA kernel: one
-    // 128-row x 128-byte box per store; CTA pairs: 32 x 32 boxes. ----
+    // ---- output: tiled map over y viewed as (M, K): one 128-row x 128-byte box per store ----
     CUtensorMap ty;
     std::memset(&ty, 0, sizeof(ty));
     {
@@ -496,10 +507,9 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
                                                               : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
         cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
         cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * eo)};
-        cuuint32_t box[2] = {use_pair ? 32u : static_cast<cuuint32_t>(128 / eo), use_pair ? 32u : 128u};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / eo), 128u};
         cuuint32_t estride[2] = {1, 1};
-        CUtensorMapSwizzle swz = use_pair ? (eo == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)
-                                          : CU_TENSOR_MAP_SWIZZLE_128B;
+        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
         CUresult cr = g_encode_tiled(&ty, dt, 2, a->y, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                      swz, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) return IMCONV_ETMAP;
@@ -522,7 +532,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     p.p = static_cast<int>(P);
     p.q = static_cast<int>(Q);
     p.m = M;
-    p.m_tiles = static_cast<int>((M + kBM * mt - 1) / (kBM * mt));
+    p.m_tiles = static_cast<int>((M + kBM * mt * (use_pair ? 2 : 1) - 1) / (kBM * mt * (use_pair ? 2 : 1)));
     p.n_tiles = static_cast<int>((K + bn - 1) / bn);
     p.rs = static_cast<int>(R * S);
     p.tps = tps;
@@ -534,6 +544,9 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     p.ldy = K;
     p.dbg = g_debug_buf;
     p.b_3d = b_3d ? 1 : 0;
+    // bf16/fp16 C = 8 with KSUB = 1 and >= 4 stages (variants 0 and 2)
+    p.a_gather = (row_bytes == 16 && E == 2 && !use_pair && variant != 1) ? 1 : 0;
+    p.x = static_cast<const uint8_t *>(a->x);
 
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
@@ -541,16 +554,16 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
 
     if (use_pair) {
         int g2 = grid;
-        if (g2 > 2 * pair_tiles) g2 = static_cast<int>(2 * pair_tiles);
+        if (g2 > 2 * tiles) g2 = static_cast<int>(2 * tiles);
         if (g2 < 2) g2 = 2;
         switch (a->in_dtype) {
             case IMCONV_BF16:
-                return a->out_dtype == IMCONV_F32 ? dispatch_bn_2sm<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
-                                                  : dispatch_bn_2sm<ELEM_BF16, OUT_BF16>(bn, ta, tb, ty, p, g2, st);
+                return a->out_dtype == IMCONV_F32 ? dispatch_bn_pair<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
+                                                  : dispatch_bn_pair<ELEM_BF16, OUT_BF16>(bn, ta, tb, ty, p, g2, st);
             case IMCONV_F16:
-                return a->out_dtype == IMCONV_F32 ? dispatch_bn_2sm<ELEM_F16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
-                                                  : dispatch_bn_2sm<ELEM_F16, OUT_F16>(bn, ta, tb, ty, p, g2, st);
-            case IMCONV_I8: return dispatch_bn_2sm<ELEM_I8, OUT_I32>(bn, ta, tb, ty, p, g2, st);
+                return a->out_dtype == IMCONV_F32 ? dispatch_bn_pair<ELEM_F16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
+                                                  : dispatch_bn_pair<ELEM_F16, OUT_F16>(bn, ta, tb, ty, p, g2, st);
+            case IMCONV_I8: return dispatch_bn_pair<ELEM_I8, OUT_I32>(bn, ta, tb, ty, p, g2, st);
             default: return IMCONV_EDTYPE;
         }
     }

@@ -107,20 +107,22 @@ def test_subtile_orders_identical(rng, order):
     assert np.array_equal(y.cpu().numpy(), want)
 
 
-def test_small_channel_tap_packing(rng):
+@pytest.mark.parametrize("flags", [0, 8, 16])  # 16-B pixels -> 0: row-band, 8: TMA taps (MT1), 16: cp.async gathers
+def test_small_channel_tap_packing(rng, flags):
     """C*elem < 128 B: several taps share one pipeline stage (16/32/64 B rows)."""
     P = _P()
     from oracle import oracle as O
     for c in (3, 8, 16, 24, 32, 40):
         x = rng.integers(-4, 5, size=(2, 15, 17, c)).astype(np.int64)
         w = rng.integers(-4, 5, size=(7, 5, c, 24)).astype(np.int64)
-        want = O.conv2d_nhwc_i64(x, w, 2, 1, 3, 2, 1, 1)
-        xb = torch.from_numpy(x).float().cuda().bfloat16()
-        wb = torch.from_numpy(w).float().cuda().bfloat16()
-        y = P._kernels.conv2d_nhwc(xb, wb, 2, 1, 3, 2, 1, 1, out_dtype=torch.float32)
-        assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), c
-        yi = P._kernels.conv2d_nhwc(x, w, 2, 1, 3, 2, 1, 1)
-        assert np.array_equal(yi, want), c
+        for args in ((2, 1, 3, 2, 1, 1), (1, 2, 2, 1, 2, 1)):
+            want = O.conv2d_nhwc_i64(x, w, *args)
+            xb = torch.from_numpy(x).float().cuda().bfloat16()
+            wb = torch.from_numpy(w).float().cuda().bfloat16()
+            y = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32, flags=flags)
+            assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), (c, args)
+            yi = P._kernels.conv2d_nhwc(x, w, *args, flags=flags)
+            assert np.array_equal(yi, want), (c, args)
 
 
 def test_gather_and_im2col_match_golden(golden):
