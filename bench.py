@@ -39,6 +39,33 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 METRIC = "conv TFLOP/s (2*N*K*C*R*S*P*Q/time)"
 
 
+def committed_traffic(config: str):
+    """DRAM bytes per step from the newest committed ncu launch list of this
+    workload (profiles/r*/launches_*.csv: dram__bytes_read + write summed over
+    the step's launches), or None."""
+    import csv
+    import glob
+    if config != "cfg4":
+        return None, None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "launches_*.csv")), key=os.path.getmtime)
+    for path in reversed(files):
+        try:
+            rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+            h = rows[0]
+            im, iv, iid = h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+            ids = set()
+            tot = 0.0
+            for r in rows[1:]:
+                ids.add(r[iid])
+                if r[im] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    tot += float(r[iv].replace(",", ""))
+            if len(ids) == 53 and tot > 0:
+                return tot, os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -404,6 +431,7 @@ def main(argv=None):
                "sample": f"{args.config}: all {len(layers_full)} layers at batch {args.cpu_sample} "
                          f"(oracle port of _fallback.conv2d_nhwc, fp32 OpenBLAS, {s:.1f} s)"}
 
+    traffic, traffic_src = committed_traffic(args.config)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -419,7 +447,11 @@ def main(argv=None):
                             "measured_burst": value / world / peaks.get("bf16_tflops", 1648.9),
                             "datasheet_2250": value / world / 2250.0},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": dtype_peak, "unit": "TFLOP/s",
-                         "frac": achieved / dtype_peak, "traffic": None,
+                         "frac": achieved / dtype_peak,
+                         "traffic": None if traffic is None else traffic / world,
+                         "traffic_unit": "DRAM bytes per step per GPU (ncu dram__bytes_read+write)",
+                         "traffic_source": traffic_src,
+                         "bytes_alg": bytes_alg_rank,
                          "peak_kind": f"{peak_kind} bf16 sustained (MEASURED_PEAKS.json)",
                          "kernel": "conv_fwd_kernel (all layers)",
                          "roofline_limited_frac": roof_ms / kern_ms},

@@ -45,9 +45,11 @@ struct RowbandParams {
     int t_min;                // min_s floor((s*dw - pw) / sw)
     int needed;               // plane pixels loaded per input row: min(Q,128) + t_max - t_min
     int plane_bytes;          // smem bytes per plane (covers 128 + t_max - t_min pixels)
-    int a_stage_bytes;        // sw * plane_bytes
+    int a_stage_bytes;        // rps * sw * plane_bytes
+    int rps;                  // input rows per pipeline stage (2: halves the per-stage handshakes)
+    int row_bytes_planes;     // sw * plane_bytes: one input row's planes
     int n_stages;
-    int in_rows;              // (TP-1)*sh + (R-1)*dh + 1
+    int in_rows;              // (TP-1)*sh + (R-1)*dh + 1, rounded up to a multiple of rps
     int npairs;
     int b_bytes;              // resident filter bytes
     int b_chunk_bytes;        // bytes of one 64-column (128 B) n-chunk of the resident filter
@@ -178,18 +180,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int n = static_cast<int>(rest / p.p_groups);
             const int col0 = p.sw * (qb * 128 + p.t_min);
             const int h0 = pg * TP * p.sh - p.ph;
-            for (int i = 0; i < p.in_rows; ++i) {
+            for (int i0 = 0; i0 < p.in_rows; i0 += p.rps) {
                 timed_wait(&empty[stage], phase ^ 1, w_empty);
-                const int h = h0 + i;
-                const bool row_ok = h >= 0 && h < p.h;
-                const uint8_t *xrow = p.x + (static_cast<size_t>(n) * p.h + (row_ok ? h : 0)) * row_bytes;
-                const uint32_t dst0 = a0 + stage * p.a_stage_bytes;
+                for (int ri = 0; ri < p.rps; ++ri) {
+                    const int h = h0 + i0 + ri;
+                    const bool row_ok = h >= 0 && h < p.h;
+                    const uint8_t *xrow = p.x + (static_cast<size_t>(n) * p.h + (row_ok ? h : 0)) * row_bytes;
+                    const uint32_t dst0 = a0 + stage * p.a_stage_bytes + ri * p.row_bytes_planes;
 #pragma unroll
-                for (int u = 0; u < kMaxEntPerThread; ++u) {
-                    if (u < n_ent) {
-                        const int col = col0 + e_col[u];
-                        const bool ok = row_ok && col >= 0 && col < p.w;
-                        ptx::cp_async_16(dst0 + e_dst[u], xrow + (ok ? col : 0) * 16, ok ? 16u : 0u);
+                    for (int u = 0; u < kMaxEntPerThread; ++u) {
+                        if (u < n_ent) {
+                            const int col = col0 + e_col[u];
+                            const bool ok = row_ok && col >= 0 && col < p.w;
+                            ptx::cp_async_16(dst0 + e_dst[u], xrow + (ok ? col : 0) * 16, ok ? 16u : 0u);
+                        }
                     }
                 }
                 ptx::cp_async_commit();
@@ -240,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < NP; ++k) adesc_r[k] = adesc_tab[k < npairs ? k : 0];
         const uint32_t stage_enc = static_cast<uint32_t>(p.a_stage_bytes >> 4);
+        const uint32_t row_enc = static_cast<uint32_t>(p.row_bytes_planes >> 4);
         ptx::mbar_wait(bfull, 0);
         int stage = 0;
         uint32_t phase = 0;
@@ -251,11 +256,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             timed_wait(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
             const uint32_t d_base = tmem_base + static_cast<uint32_t>(acc * TP * BN);
-            for (int i = 0; i < p.in_rows; ++i) {
+            for (int i0 = 0; i0 < p.in_rows; i0 += p.rps) {
                 timed_wait(&full[stage], phase, w_full);
                 ptx::tc_fence_after();
-                {
-                    const uint64_t a_add = static_cast<uint64_t>(stage * stage_enc);
+                for (int ri = 0; ri < p.rps; ++ri) {
+                    const int i = i0 + ri;
+                    const uint64_t a_add = static_cast<uint64_t>(stage * stage_enc + ri * row_enc);
                     int rrs[TP];
 #pragma unroll
                     for (int j = 0; j < TP; ++j) rrs[j] = rr_tab[i * TP + j];
@@ -272,8 +278,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                    (rr | pr) != 0 ? 1u : 0u);
                         }
                     }
-                    ptx::mma_commit_elect(&empty[stage]);
                 }
+                ptx::mma_commit_elect(&empty[stage]);
                 if (++stage == p.n_stages) {
                     stage = 0;
                     phase ^= 1;

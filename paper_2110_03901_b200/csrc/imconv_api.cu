@@ -238,8 +238,11 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     p.dbg = g_debug_buf;
     p.dbg_flags = g_debug_flags;
     p.plane_bytes = ((plane_pix * 16 + 127) / 128) * 128;
-    p.a_stage_bytes = p.sw * p.plane_bytes;
+    p.rps = 2;  // two input rows per stage: halves the MMA issuer's per-stage handshakes
+    p.row_bytes_planes = p.sw * p.plane_bytes;
+    p.a_stage_bytes = p.rps * p.row_bytes_planes;
     p.in_rows = (TP - 1) * p.sh + (R - 1) * p.dh + 1;
+    p.in_rows = (p.in_rows + p.rps - 1) / p.rps * p.rps;
     p.npairs = (S + 1) / 2;
     p.b_chunk_bytes = R * p.npairs * 2 * 1024;
     p.b_bytes = (BN / 64) * p.b_chunk_bytes;
