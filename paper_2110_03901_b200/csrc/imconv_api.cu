@@ -416,6 +416,10 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
 
     const int bn = pick_bn(a->in_dtype, K, a->tile_n);
     if (bn < 0) return IMCONV_EINVAL;
+    // (A wave-quantisation chooser over {256x128, 128x256, 128x128, ...} blocks
+    // was measured worse on the stage-5 layers: smaller blocks lose more
+    // per-block efficiency than they gain in wave fill, so BN is fixed by K.)
+    const int auto_variant = -1;
 
     // ---- block shape: single CTA or CTA pair (cta_group::2, B split across the pair) ----
     // pairs need whole swizzle-atom columns per CTA (BN >= 128 bf16 / 256 int8)
@@ -430,7 +434,8 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     const bool use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && (a->flags & IMCONV_FLAG_CTA_PAIR) &&
                           pair_tiles >= 1;
     // single-CTA block shape (see dispatch_bn): N <= 128 -> 2 m-tiles per CTA
-    const int variant = (a->flags & IMCONV_FLAG_KSUB1) ? 2 : (a->flags & IMCONV_FLAG_MT1) ? 1 : 0;
+    const int variant = auto_variant >= 0 ? auto_variant
+                        : (a->flags & IMCONV_FLAG_KSUB1) ? 2 : (a->flags & IMCONV_FLAG_MT1) ? 1 : 0;
     const int mt = (!use_pair && bn <= 128 && variant == 0) ? 2 : 1;
 
     // ---- A operand: im2col tensor map over NHWC ----
