@@ -28,8 +28,9 @@ __global__ void im2col_cf_vec16_kernel(const uint4 *__restrict__ x, uint4 *__res
         const int pqr = static_cast<int>(m - n * pq);
         const int op = pqr / q_;
         const int oq = pqr - op * q_;
-        const int tap_r = taps == 1 ? r_lo : t / wf;
-        const int tap_s = taps == 1 ? s_lo : t - (t / wf) * wf;
+        // r_lo >= 0: single fixed tap (tile gather); else tap t of a full im2col (t = 0 when hf*wf == 1)
+        const int tap_r = r_lo >= 0 ? r_lo : t / wf;
+        const int tap_s = r_lo >= 0 ? s_lo : t - (t / wf) * wf;
         const int hh = op * sh + tap_r * dh - ph;
         const int ww = oq * sw + tap_s * dw - pw;
         uint4 v = make_uint4(0, 0, 0, 0);

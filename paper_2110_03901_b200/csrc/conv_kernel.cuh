@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         uint32_t chunk_ctr = 0;
-        long long w_tfull = 0;
+        long long w_tfull = 0, t_ld = 0, t_bar = 0, t_st = 0;
         const long long t_start = clock64();
         for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
             const long long m_tile = tile / p.n_tiles;
@@ -632,17 +632,26 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                     uint32_t v[kOC];
                     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                            static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC);
+                    const long long e0 = IMCONV_INSTRUMENT ? clock64() : 0;
 #pragma unroll
                     for (int h = 0; h < kOC / 32; ++h)
                         ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
                     ptx::tmem_ld_wait();
+                    const long long e1 = IMCONV_INSTRUMENT ? clock64() : 0;
                     if (col0 >= p.k || row0 >= p.m) continue;  // uniform over the 4 warps
                     uint8_t *buf = smem_out + (chunk_ctr & 1) * Cfg::kOutTile;
                     if (issuer) ptx::tma_store_wait_read<1>();  // the store issued 2 chunks ago has read buf
                     ptx::named_bar_sync(1, 128);
+                    const long long e2 = IMCONV_INSTRUMENT ? clock64() : 0;
                     stage_row128<OUT>(buf, row, v);
                     ptx::fence_proxy_async_smem();
+                    const long long e3 = IMCONV_INSTRUMENT ? clock64() : 0;
                     ptx::named_bar_sync(1, 128);
+                    if (IMCONV_INSTRUMENT) {
+                        t_ld += e1 - e0;
+                        t_bar += (e2 - e1) + (clock64() - e3);
+                        t_st += e3 - e2;
+                    }
                     if (issuer) {
                         ptx::tma_store_2d(&tmap_y, buf, col0, static_cast<int>(row0));  // clipped at M / K
                         ptx::tma_store_commit();
@@ -666,6 +675,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         if (IMCONV_INSTRUMENT && p.dbg && lane == 0 && quarter == 0) {
             p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 6] = w_tfull;
+            p.dbg[blockIdx.x * 8 + 7] = t_ld;
+            p.dbg[148 * 8 + blockIdx.x * 2 + 0] = t_bar;
+            p.dbg[148 * 8 + blockIdx.x * 2 + 1] = t_st;
         }
     }
 

@@ -146,6 +146,12 @@ def test_im2col_vector_path_bf16(rng):
     got = P._kernels.im2col_nhwc(x.cuda(), 3, 3, 2, 2, 1, 1, 1, 1, True).cpu()
     want = O.im2col_nhwc(x.view(torch.int16).numpy(), 3, 3, 2, 2, 1, 1, 1, 1, True)
     assert np.array_equal(got.view(torch.int16).numpy(), want)
+    # 1x1 filters (single tap, full lowering) and a 1xS filter through the vector path
+    for hf, wf, st, pd in ((1, 1, 1, 0), (1, 1, 2, 0), (1, 3, 1, 1), (7, 7, 2, 3)):
+        got = P._kernels.im2col_nhwc(x.cuda(), hf, wf, st, st, pd, pd, 1, 1, True).cpu()
+        want = O.im2col_nhwc(x.view(torch.int16).numpy(), hf, wf, st, st, pd, pd, 1, 1, True)
+        assert np.array_equal(got.view(torch.int16).numpy(), want), (hf, wf, st, pd)
+    assert torch.equal(P._kernels.im2col_nhwc(x.cuda(), 1, 1, 1, 1, 0, 0, 1, 1, True).cpu(), x.reshape(-1, 64))
 
 
 def test_explicit_path_equals_implicit(golden):

@@ -71,15 +71,17 @@ def main():
     ms = ev[0].elapsed_time(ev[1]) / args.reps
     print(f"{args.layer} n={sp.n}: {ms:.4f} ms  {sp.flops / ms / 1e9:.1f} TFLOP/s")
     if args.waits:
-        dbg = torch.zeros(148 * 8, dtype=torch.int64, device=dev)
+        dbg = torch.zeros(148 * 10, dtype=torch.int64, device=dev)
         _lib.lib.imconv_debug_set_buffer(dbg.data_ptr())
         conv_device(x, w, *sp.conv_args(), tile_n=args.tile_n, order=order)
         torch.cuda.synchronize()
         _lib.lib.imconv_debug_set_buffer(None)
-        d = dbg.view(148, 8).double().mean(0).tolist()
+        d = dbg[:148 * 8].view(148, 8).double().mean(0).tolist()
         names = ["prod_total", "prod_wait_empty", "mma_total", "mma_wait_tempty", "mma_wait_full",
-                 "epi_total", "epi_wait_tfull", "-"]
+                 "epi_total", "epi_wait_tfull", "epi_tmem_ld"]
         print("  ".join(f"{nm}={v / 1e3:.1f}k" for nm, v in zip(names, d)))
+        e = dbg[148 * 8:].view(148, 2).double().mean(0).tolist()
+        print(f"  epi_barriers+store_waits={e[0] / 1e3:.1f}k  epi_smem_staging={e[1] / 1e3:.1f}k")
 
 
 if __name__ == "__main__":
