@@ -275,7 +275,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
-    const int warp = threadIdx.x >> 5;
+    // broadcast from lane 0: the role branches are then provably warp-uniform and
+    // ptxas keeps the MMA issuer's descriptors on the uniform datapath
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const uint32_t lane = threadIdx.x & 31;
     const long long total_tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;  // m_tiles of CG*kRows pixels
     const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;  // 0 = leader (issues the MMAs)
@@ -676,8 +678,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 6] = w_tfull;
             p.dbg[blockIdx.x * 8 + 7] = t_ld;
-            p.dbg[148 * 8 + blockIdx.x * 2 + 0] = t_bar;
-            p.dbg[148 * 8 + blockIdx.x * 2 + 1] = t_st;
+            p.dbg[148 * 8 + blockIdx.x * 4 + 0] = t_bar;
+            p.dbg[148 * 8 + blockIdx.x * 4 + 1] = t_st;
         }
     }
 

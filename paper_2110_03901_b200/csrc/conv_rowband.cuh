@@ -33,8 +33,8 @@
 namespace imconv {
 
 constexpr int kMaxPairs = 8;  // S <= 16
-constexpr int kProducers = 64;  // warps 2-3 gather the planes
-constexpr int kMaxEntPerThread = 8;  // sw * needed <= 512 plane pixels per input row
+constexpr int kProducers = 128;  // warps 0, 2, 3 and 8 gather the planes
+constexpr int kMaxEntPerThread = 4;  // sw * needed <= 512 plane pixels per input row
 
 struct RowbandParams {
     int n, h, w, k;
@@ -60,17 +60,24 @@ struct RowbandParams {
     const uint8_t *x;         // NHWC input, 16 bytes per pixel
     long long *dbg;           // optional per-CTA wait-cycle counters (instrumentation), else nullptr
     int dbg_flags;            // instrumentation: 1 = epilogue skips TMEM/stores, 2 = producer skips copies,
-                              // 4 = one MMA per (row, filter row) instead of npairs
+                              // 4 = one MMA per (row, filter row) instead of npairs, 8 = issuer skips MMAs,
+                              // 16 = producer skips the proxy fence, 32 = one full-barrier arrive per warp,
+                              // 64 / 128 = epilogue / producer waits back off with nanosleep
 };
 
 // instrumentation: cycles spent in a blocking wait, accumulated per role
-__device__ __forceinline__ void timed_wait(uint64_t *bar, uint32_t parity, long long &acc) {
+__device__ __forceinline__ void timed_wait(uint64_t *bar, uint32_t parity, long long &acc, int sleep_ns = 0) {
 #if IMCONV_INSTRUMENT
     const long long t0 = clock64();
-    ptx::mbar_wait(bar, parity);
+    if (sleep_ns) {
+        while (!ptx::mbar_try_wait(ptx::smem_u32(bar), parity)) __nanosleep(sleep_ns);
+    } else {
+        ptx::mbar_wait(bar, parity);
+    }
     acc += clock64() - t0;
 #else
     (void)acc;
+    (void)sleep_ns;
     ptx::mbar_wait(bar, parity);
 #endif
 }
@@ -85,7 +92,7 @@ struct RowbandCfg {
 };
 
 template <int ELEM, int OUT, int BN, int TP, int NP>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsGeneric, 1)
     conv_rowband_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_y,
                         const RowbandParams p) {
     using Cfg = RowbandCfg<ELEM, OUT, BN, TP>;
@@ -104,14 +111,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *adesc_tab = reinterpret_cast<uint64_t *>(tmem_slot + 2);          // kMaxPairs entries
     int8_t *rr_tab = reinterpret_cast<int8_t *>(adesc_tab + kMaxPairs);         // in_rows * TP entries (<= 256)
 
-    const int warp = threadIdx.x >> 5;
+    // broadcast from lane 0: the role branches are then provably warp-uniform and
+    // ptxas keeps the MMA issuer's descriptors on the uniform datapath
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const uint32_t lane = threadIdx.x & 31;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_w);
         ptx::prefetch_tmap(&tmap_y);
         for (int i = 0; i < p.n_stages; ++i) {
-            ptx::mbar_init(&full[i], kProducers);  // one arrival per plane-producer thread
+            // one arrival per plane-producer thread (instrumentation flag 32: per warp)
+            ptx::mbar_init(&full[i], (IMCONV_INSTRUMENT && (p.dbg_flags & 32)) ? kProducers / 32 : kProducers);
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -145,11 +155,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
         }
         __syncwarp();
-    } else if (warp == 2 || warp == 3) {
+    }
+    if (warp == 0 || warp == 2 || warp == 3 || warp == 8) {
         // ---- plane producers: cp.async 16-byte pixels into the stride-phase planes ----
         // (LSU path: a 16-byte TMA element costs as much TMA time as a 128-byte
-        // one, so strided 16-byte pixels are gathered by threads instead)
-        const int t = threadIdx.x - 64;
+        // one, so strided 16-byte pixels are gathered by threads instead; warp 0
+        // joins after issuing the resident-filter load)
+        const int t = (warp == 0 ? 0 : warp == 8 ? 3 : warp - 1) * 32 + static_cast<int>(lane);
         const int entries = (IMCONV_INSTRUMENT && (p.dbg_flags & 2)) ? 0 : p.sw * p.needed;
         const uint32_t a0 = ptx::smem_u32(smem_a);
         // this thread's (plane, pixel) entries, fixed for the whole kernel:
@@ -166,13 +178,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             n_ent += k < entries ? 1 : 0;
         }
         const size_t row_bytes = static_cast<size_t>(p.w) * 16;
-        constexpr int kLag = 4;  // cp.async groups kept in flight per thread
-        int pend[kLag + 1];
-        int npend = 0;
+        // cp.async groups (stages) kept in flight per thread; must stay below
+        // n_stages - 1 or the arrival for a stage would wait on its own slot
+        constexpr int kLag = 4;
+        const int lag = p.n_stages - 2 < kLag ? p.n_stages - 2 : kLag;
+        int npend = 0;      // committed cp.async groups not yet signalled
+        int arr_stage = 0;  // oldest of them (stages are committed and signalled in ring order)
         int stage = 0;
         uint32_t phase = 0;
-        long long w_empty = 0;
+        long long w_empty = 0, t_wg = 0, t_fa = 0;
         const long long t_start = clock64();
+        auto signal_oldest = [&]() {
+            if (IMCONV_INSTRUMENT && (p.dbg_flags & 32)) {
+                __syncwarp();
+                if ((t & 31) == 0) ptx::mbar_arrive(&full[arr_stage]);
+            } else {
+                ptx::mbar_arrive(&full[arr_stage]);
+            }
+            if (++arr_stage == p.n_stages) arr_stage = 0;
+            --npend;
+        };
         for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
             const int qb = static_cast<int>(tile % p.q_blocks);
             const long long rest = tile / p.q_blocks;
@@ -180,30 +205,52 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int n = static_cast<int>(rest / p.p_groups);
             const int col0 = p.sw * (qb * 128 + p.t_min);
             const int h0 = pg * TP * p.sh - p.ph;
+            // per-tile column validity of this thread's entries (rows are checked per row)
+            uint32_t col_ok = 0;
+            int e_src[kMaxEntPerThread];
+#pragma unroll
+            for (int u = 0; u < kMaxEntPerThread; ++u) {
+                const int col = col0 + e_col[u];
+                const bool ok = u < n_ent && col >= 0 && col < p.w;
+                col_ok |= ok ? (1u << u) : 0u;
+                e_src[u] = (ok ? col : 0) * 16;
+            }
             for (int i0 = 0; i0 < p.in_rows; i0 += p.rps) {
-                timed_wait(&empty[stage], phase ^ 1, w_empty);
+                timed_wait(&empty[stage], phase ^ 1, w_empty, (p.dbg_flags & 128) ? 100 : 0);
                 for (int ri = 0; ri < p.rps; ++ri) {
                     const int h = h0 + i0 + ri;
                     const bool row_ok = h >= 0 && h < p.h;
                     const uint8_t *xrow = p.x + (static_cast<size_t>(n) * p.h + (row_ok ? h : 0)) * row_bytes;
                     const uint32_t dst0 = a0 + stage * p.a_stage_bytes + ri * p.row_bytes_planes;
+                    const uint32_t ok_mask = row_ok ? col_ok : 0u;
 #pragma unroll
                     for (int u = 0; u < kMaxEntPerThread; ++u) {
-                        if (u < n_ent) {
-                            const int col = col0 + e_col[u];
-                            const bool ok = row_ok && col >= 0 && col < p.w;
-                            ptx::cp_async_16(dst0 + e_dst[u], xrow + (ok ? col : 0) * 16, ok ? 16u : 0u);
-                        }
+                        if (u < n_ent)
+                            ptx::cp_async_16(dst0 + e_dst[u], xrow + e_src[u], ((ok_mask >> u) & 1u) ? 16u : 0u);
                     }
                 }
                 ptx::cp_async_commit();
-                pend[npend++] = stage;
-                if (npend > kLag) {
-                    ptx::cp_async_wait<kLag>();
-                    ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05 (async proxy)
-                    ptx::mbar_arrive(&full[pend[0]]);
-                    for (int u = 0; u < kLag; ++u) pend[u] = pend[u + 1];
-                    --npend;
+                ++npend;
+                if (npend > lag) {
+#if IMCONV_INSTRUMENT
+                    const long long tw0 = clock64();
+#endif
+                    switch (lag) {  // wait_group takes an immediate
+                        case 1: ptx::cp_async_wait<1>(); break;
+                        case 2: ptx::cp_async_wait<2>(); break;
+                        case 3: ptx::cp_async_wait<3>(); break;
+                        default: ptx::cp_async_wait<kLag>(); break;
+                    }
+#if IMCONV_INSTRUMENT
+                    const long long tw1 = clock64();
+                    t_wg += tw1 - tw0;
+#endif
+                    if (!(IMCONV_INSTRUMENT && (p.dbg_flags & 16)))
+                        ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05 (async proxy)
+                    signal_oldest();
+#if IMCONV_INSTRUMENT
+                    t_fa += clock64() - tw1;
+#endif
                 }
                 if (++stage == p.n_stages) {
                     stage = 0;
@@ -213,10 +260,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::cp_async_wait<0>();
         ptx::fence_proxy_async_smem();
-        for (int u = 0; u < npend; ++u) ptx::mbar_arrive(&full[pend[u]]);
+        while (npend > 0) signal_oldest();
         if (IMCONV_INSTRUMENT && p.dbg && t == 0) {
             p.dbg[blockIdx.x * 8 + 0] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 1] = w_empty;
+            p.dbg[148 * 8 + blockIdx.x * 4 + 2] = t_fa;
+            p.dbg[148 * 8 + blockIdx.x * 4 + 3] = t_wg;
         }
     } else if (warp == 1) {
         // ---- MMA issuer ----
@@ -231,18 +280,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             rr = (rr >= 0 && rr % p.dh == 0 && rr / p.dh < p.r) ? rr / p.dh : -1;
             rr_tab[u] = static_cast<int8_t>(rr);
         }
-        if (lane < p.npairs)
-            adesc_tab[lane] = ptx::smem_desc(ptx::smem_u32(smem_a) + p.pair_a_off[lane], p.pair_lbo[lane], 128,
-                                             ptx::LAYOUT_NONE);
-        __syncwarp();
-        const uint64_t bdesc0 = ptx::smem_desc(ptx::smem_u32(smem_b), p.b_chunk_bytes, 1024, ptx::LAYOUT_SW128);
-        const int npairs = (IMCONV_INSTRUMENT && (p.dbg_flags & 4)) ? 1 : p.npairs;
-        // register-resident pair descriptors (NP >= npairs, compile-time bound):
-        // the MMA asm statements clobber memory, so table reads from smem would
-        // otherwise be re-issued (and waited on) before every MMA
+        // Every operand below is provably warp-uniform (kernel parameters,
+        // uniform loop counters, and values broadcast from lane 0 with
+        // __shfl_sync), so ptxas keeps the descriptors in uniform registers and
+        // each MMA is ~2 uniform adds + UTCHMMA -- no per-MMA elect / R2UR
+        // broadcast, which otherwise made this single issuing warp (not the
+        // tensor pipe) the stem's bottleneck at ~100 cycles per MMA.
+        const uint32_t a_base = __shfl_sync(0xffffffffu, ptx::smem_u32(smem_a), 0);
+        const uint32_t b_base = __shfl_sync(0xffffffffu, ptx::smem_u32(smem_b), 0);
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
+        const int npairs = (IMCONV_INSTRUMENT && (p.dbg_flags & 8)) ? 0 : (IMCONV_INSTRUMENT && (p.dbg_flags & 4)) ? 1 : p.npairs;
         uint64_t adesc_r[NP];
 #pragma unroll
-        for (int k = 0; k < NP; ++k) adesc_r[k] = adesc_tab[k < npairs ? k : 0];
+        for (int k = 0; k < NP; ++k) {
+            const int kk = k < p.npairs ? k : 0;
+            adesc_r[k] = ptx::smem_desc(a_base + p.pair_a_off[kk], p.pair_lbo[kk], 128, ptx::LAYOUT_NONE);
+        }
+        const uint64_t bdesc0 = ptx::smem_desc(b_base, p.b_chunk_bytes, 1024, ptx::LAYOUT_SW128);
         const uint32_t stage_enc = static_cast<uint32_t>(p.a_stage_bytes >> 4);
         const uint32_t row_enc = static_cast<uint32_t>(p.row_bytes_planes >> 4);
         ptx::mbar_wait(bfull, 0);
@@ -250,21 +304,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        long long w_tempty = 0, w_full = 0;
+        long long w_tempty = 0, w_full = 0, t_loop = 0, t_commit = 0;
         const long long t_start = clock64();
         for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
             timed_wait(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
-            const uint32_t d_base = tmem_base + static_cast<uint32_t>(acc * TP * BN);
+            const uint32_t d_base = tmem_u + static_cast<uint32_t>(acc * TP * BN);
             for (int i0 = 0; i0 < p.in_rows; i0 += p.rps) {
                 timed_wait(&full[stage], phase, w_full);
                 ptx::tc_fence_after();
+#if IMCONV_INSTRUMENT
+                const long long tm0 = clock64();
+#endif
                 for (int ri = 0; ri < p.rps; ++ri) {
                     const int i = i0 + ri;
                     const uint64_t a_add = static_cast<uint64_t>(stage * stage_enc + ri * row_enc);
                     int rrs[TP];
+                    if (p.dh == 1) {  // filter row of output row j fed by input row i (no table read)
 #pragma unroll
-                    for (int j = 0; j < TP; ++j) rrs[j] = rr_tab[i * TP + j];
+                        for (int j = 0; j < TP; ++j) {
+                            const int rr = i - j * p.sh;
+                            rrs[j] = (rr >= 0 && rr < p.r) ? rr : -1;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < TP; ++j) rrs[j] = __shfl_sync(0xffffffffu, rr_tab[i * TP + j], 0);
+                    }
 #pragma unroll
                     for (int j = 0; j < TP; ++j) {
                         const int rr = rrs[j];
@@ -279,7 +344,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+#if IMCONV_INSTRUMENT
+                const long long tm1 = clock64();
+                t_loop += tm1 - tm0;
+#endif
                 ptx::mma_commit_elect(&empty[stage]);
+#if IMCONV_INSTRUMENT
+                t_commit += clock64() - tm1;
+#endif
                 if (++stage == p.n_stages) {
                     stage = 0;
                     phase ^= 1;
@@ -293,7 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.dbg[blockIdx.x * 8 + 2] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 3] = w_tempty;
             p.dbg[blockIdx.x * 8 + 4] = w_full;
-
+            p.dbg[148 * 8 + blockIdx.x * 4 + 0] = t_commit;
+            p.dbg[148 * 8 + blockIdx.x * 4 + 1] = t_loop;
         }
     } else if (warp >= 4) {
         // ---- epilogue: TP accumulators -> NHWC via 4-D TMA stores ----
@@ -311,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int pg = static_cast<int>(rest % p.p_groups);
             const int n = static_cast<int>(rest / p.p_groups);
             const int qrow = qb * 128 + quarter * 32;
-            timed_wait(&tfull[acc], acc_phase, w_tfull);
+            timed_wait(&tfull[acc], acc_phase, w_tfull, (p.dbg_flags & 64) ? 200 : 0);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int j = 0; j < TP; ++j) {

@@ -187,7 +187,7 @@ int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandPa
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid, kThreads, smem, st>>>(tw, ty, p);
+    kern<<<grid, kThreadsGeneric, smem, st>>>(tw, ty, p);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
@@ -238,14 +238,29 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     p.dbg = g_debug_buf;
     p.dbg_flags = g_debug_flags;
     p.plane_bytes = ((plane_pix * 16 + 127) / 128) * 128;
-    p.rps = 2;  // two input rows per stage: halves the MMA issuer's per-stage handshakes
     p.row_bytes_planes = p.sw * p.plane_bytes;
-    p.a_stage_bytes = p.rps * p.row_bytes_planes;
-    p.in_rows = (TP - 1) * p.sh + (R - 1) * p.dh + 1;
-    p.in_rows = (p.in_rows + p.rps - 1) / p.rps * p.rps;
+    const int rows_needed = (TP - 1) * p.sh + (R - 1) * p.dh + 1;
     p.npairs = (S + 1) / 2;
     p.b_chunk_bytes = R * p.npairs * 2 * 1024;
     p.b_bytes = (BN / 64) * p.b_chunk_bytes;
+    const int kStageOut = 2 * 32 * ((a->out_dtype == IMCONV_F32) ? 128 : 64);
+    const int fixed = p.b_bytes + 4 * kStageOut + 1024 /*align*/ + 1024 /*barriers + tables*/;
+    const int room = kMaxDynSmem - fixed;
+    // input rows per pipeline stage: every stage costs the MMA issuer a fixed
+    // handshake (wait, fences, commit), so stages are made as large as the
+    // ring allows while keeping >= kMinStages of them in flight
+    constexpr int kMinStages = 4;
+    p.rps = 1;
+    for (int spb = 1; spb <= rows_needed; ++spb) {  // fewest stages per block, then fewest padding rows
+        const int rps = (rows_needed + spb - 1) / spb;
+        if (room / (rps * p.row_bytes_planes) >= kMinStages) {
+            p.rps = rps;
+            break;
+        }
+    }
+    if (g_debug_flags >> 8) p.rps = std::min(rows_needed, g_debug_flags >> 8);  // experiment override
+    p.a_stage_bytes = p.rps * p.row_bytes_planes;
+    p.in_rows = (rows_needed + p.rps - 1) / p.rps * p.rps;
     // taps ordered by their run address inside a stage, paired neighbour-wise
     int order[2 * kMaxPairs], addr[2 * kMaxPairs];
     for (int s = 0; s < S; ++s) {
@@ -261,9 +276,6 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
         p.pair_a_off[pr] = addr[s0];
         p.pair_lbo[pr] = s1 >= 0 ? addr[s1] - addr[s0] : 16;  // zero tap: any finite run
     }
-    const int kStageOut = 2 * 32 * ((a->out_dtype == IMCONV_F32) ? 128 : 64);
-    const int fixed = p.b_bytes + 4 * kStageOut + 1024 /*align*/ + 1024 /*barriers + tables*/;
-    const int room = kMaxDynSmem - fixed;
     p.n_stages = std::min(24, room / p.a_stage_bytes);
     if (p.b_bytes > 128 * 1024 || p.n_stages < 3 || p.in_rows * TP > 256 || 2 * p.n_stages * 8 + 64 > 512 ||
         p.sw * p.needed > kProducers * kMaxEntPerThread)

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--explicit", action="store_true", help="K3 im2col + K4 GEMM instead of the implicit kernel")
     ap.add_argument("--waits", action="store_true", help="print per-role wait-cycle instrumentation")
     ap.add_argument("--dbg-flags", type=int, default=0, help="instrumentation: disable kernel roles (wrong results)")
+    ap.add_argument("--rps", type=int, default=0, help="row-band kernel: input rows per stage override (0 = auto)")
     args = ap.parse_args()
     if args.waits or args.dbg_flags:
         os.environ["IMCONV_INSTRUMENTED"] = "1"
@@ -44,7 +45,7 @@ def main():
         x = torch.randn((sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev).to(torch.bfloat16)
         w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev) * 0.05).to(torch.bfloat16)
     order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[args.order]
-    _lib.lib.imconv_debug_set_flags(args.dbg_flags)
+    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8))
     def once():
         if args.explicit:
             low = K.im2col_nhwc(x, sp.h_f, sp.w_f, *sp.conv_args(), True)
@@ -71,7 +72,7 @@ def main():
     ms = ev[0].elapsed_time(ev[1]) / args.reps
     print(f"{args.layer} n={sp.n}: {ms:.4f} ms  {sp.flops / ms / 1e9:.1f} TFLOP/s")
     if args.waits:
-        dbg = torch.zeros(148 * 10, dtype=torch.int64, device=dev)
+        dbg = torch.zeros(148 * 12, dtype=torch.int64, device=dev)
         _lib.lib.imconv_debug_set_buffer(dbg.data_ptr())
         conv_device(x, w, *sp.conv_args(), tile_n=args.tile_n, order=order)
         torch.cuda.synchronize()
@@ -80,8 +81,9 @@ def main():
         names = ["prod_total", "prod_wait_empty", "mma_total", "mma_wait_tempty", "mma_wait_full",
                  "epi_total", "epi_wait_tfull", "epi_tmem_ld"]
         print("  ".join(f"{nm}={v / 1e3:.1f}k" for nm, v in zip(names, d)))
-        e = dbg[148 * 8:].view(148, 2).double().mean(0).tolist()
-        print(f"  epi_barriers+store_waits={e[0] / 1e3:.1f}k  epi_smem_staging={e[1] / 1e3:.1f}k")
+        e = dbg[148 * 8:].view(148, 4).double().mean(0).tolist()
+        print("  extra (generic: epi barriers+store waits, epi staging; row-band: issuer commit, issuer mma loop, "
+              "producer fence+arrive, producer wait_group): " + "  ".join(f"{v / 1e3:.1f}k" for v in e))
 
 
 if __name__ == "__main__":
