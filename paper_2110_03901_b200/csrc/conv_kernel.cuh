@@ -533,9 +533,15 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             a_kk[kk] = off >> 4;
         }
         const uint32_t a_mt = static_cast<uint32_t>((kBM * rb) >> 4);  // m-tile step inside a tap block
-        const uint64_t adesc0 = ptx::smem_desc(ptx::smem_u32(smem_a), a_lbo, a_sbo, a_layout);
-        const uint64_t bdesc0 =
-            ptx::smem_desc(ptx::smem_u32(smem_b), Cfg::kBKE * kRowBytes, 1024, ptx::LAYOUT_SW128);
+        // The whole warp runs the issue loop on warp-uniform values (lane-0
+        // broadcasts below) and one elected lane issues each MMA: ptxas then
+        // keeps every descriptor in uniform registers (no per-MMA R2UR
+        // broadcast / single-lane waterfall loop around each UTCHMMA).
+        const uint64_t adesc0 =
+            ptx::smem_desc(__shfl_sync(0xffffffffu, ptx::smem_u32(smem_a), 0), a_lbo, a_sbo, a_layout);
+        const uint64_t bdesc0 = ptx::smem_desc(__shfl_sync(0xffffffffu, ptx::smem_u32(smem_b), 0),
+                                               Cfg::kBKE * kRowBytes, 1024, ptx::LAYOUT_SW128);
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -545,11 +551,11 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
             timed_wait_g(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
-            const uint32_t d_base = tmem_base + static_cast<uint32_t>(acc * MT * BN);
+            const uint32_t d_base = tmem_u + static_cast<uint32_t>(acc * MT * BN);
             for (int kb = 0; kb < k_stages; ++kb) {
                 timed_wait_g(&full[stage], phase, w_full);
                 ptx::tc_fence_after();
-                if (lane == 0) {
+                {
                     const int nsub = min(KSUB, k_subs - kb * KSUB);
                     const uint64_t a_st = adesc0 + static_cast<uint64_t>((stage * Cfg::kAStageK) >> 4);
                     const uint64_t b_st = bdesc0 + static_cast<uint64_t>((stage * Cfg::kBStage) >> 4);
@@ -567,13 +573,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                                         a_st + static_cast<uint64_t>((u * Cfg::kASub) >> 4) + mt * a_mt + a_kk[kk];
                                     if constexpr (CG == 2) {
                                         if constexpr (ELEM == ELEM_I8)
-                                            ptx::mma_i8_2sm(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                            ptx::mma_i8_2sm_elect(d_base + mt * BN, adesc, bdesc, idesc, accum);
                                         else
-                                            ptx::mma_f16_2sm(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                            ptx::mma_f16_2sm_elect(d_base + mt * BN, adesc, bdesc, idesc, accum);
                                     } else if constexpr (ELEM == ELEM_I8) {
-                                        ptx::mma_i8(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                        ptx::mma_i8_elect(d_base + mt * BN, adesc, bdesc, idesc, accum);
                                     } else {
-                                        ptx::mma_f16(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                        ptx::mma_f16_elect(d_base + mt * BN, adesc, bdesc, idesc, accum);
                                     }
                                 }
                             }
@@ -581,23 +587,20 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                     }
                     // frees the smem slot (in both CTAs of a pair) once these MMAs retire
                     if constexpr (CG == 2)
-                        ptx::mma_commit_2sm(&empty[stage]);
+                        ptx::mma_commit_2sm_elect(&empty[stage]);
                     else
-                        ptx::mma_commit(&empty[stage]);
+                        ptx::mma_commit_elect(&empty[stage]);
                 }
-                __syncwarp();
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (lane == 0) {  // accumulators complete -> epilogue(s)
-                if constexpr (CG == 2)
-                    ptx::mma_commit_2sm(&tfull[acc]);
-                else
-                    ptx::mma_commit(&tfull[acc]);
-            }
-            __syncwarp();
+            // accumulators complete -> epilogue(s)
+            if constexpr (CG == 2)
+                ptx::mma_commit_2sm_elect(&tfull[acc]);
+            else
+                ptx::mma_commit_elect(&tfull[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
