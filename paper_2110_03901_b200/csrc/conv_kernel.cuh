@@ -41,7 +41,8 @@ constexpr int kBM = 128;           // output pixels per block (MMA M)
 constexpr int kRowBytes = 128;     // bytes of reduction per stage per row (one 128B swizzle span)
 constexpr int kAStage = kBM * kRowBytes;  // 16 KiB of A per stage
 constexpr int kThreads = 256;
-constexpr int kThreadsGeneric = 288;  // + warp 8: second filter producer
+constexpr int kThreadsRowband = 288;  // conv_rowband_kernel: 4 plane-producer warps (0, 2, 3, 8), issuer, 4 epilogue warps
+constexpr int kThreadsGeneric = 320;  // + warp 8: second filter producer, warp 9: output store issuer
 
 enum ElemKind : int { ELEM_BF16 = 0, ELEM_F16 = 1, ELEM_I8 = 2 };
 enum OutKind : int { OUT_BF16 = 0, OUT_F16 = 1, OUT_F32 = 2, OUT_I32 = 3 };
@@ -67,6 +68,10 @@ struct ConvParams {
     int b_3d;            // 1: the filter map is 3-D {chunk cols, rows, chunks}: one TMA per stage for all of B
     int a_gather;        // 1: 16-byte pixels -- A tap blocks gathered by cp.async warps instead of TMA
     const uint8_t *x;    // NHWC input (gather mode)
+    int a_tiled;         // 1: 1x1 / stride 1 / no padding -- A is the plain (M x C) matrix, loaded with
+                         //    tiled TMA boxes {128 B of channels, rows} (cheaper per operation than im2col)
+    int dbg_flags;       // instrumentation builds only: 1 / 2 = load B / A on a CTA's first tile only
+                         // (wrong results; measures what the operand stream costs)
 };
 
 // Division-free walk over the k-subtiles (filter tap <r,s>, channel chunk) of
@@ -236,8 +241,9 @@ struct ConvCfg {
     static constexpr int kOutCols = (OUT == OUT_BF16 || OUT == OUT_F16) ? 64 : 32;
     static constexpr int kOutTile = kBM * 128;
     static constexpr int kStageOut = 2 * 32 * OutTraits<OUT>::kRowBytes;  // (CTA-pair kernel)
+    static constexpr int kOutTiles = 2;             // double-buffered epilogue staging
     static constexpr int kSmemBytes =
-        STAGES * (kAStageK + kBStage) + 2 * kOutTile + 1024 /*align*/ + 256 /*barriers*/;
+        STAGES * (kAStageK + kBStage) + kOutTiles * kOutTile + 1024 /*align*/ + 256 /*barriers*/;
     static_assert((BN / CG) % kNC == 0, "each CTA must hold whole swizzle-atom columns of B");
     static_assert(CG == 1 || (MT == 1 && KSUB == 1), "CTA pairs run one m-tile and one k-subtile per stage");
     static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
@@ -268,7 +274,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     uint8_t *smem_a = smem;
     uint8_t *smem_b = smem + STAGES * Cfg::kAStageK;
     uint8_t *smem_out = smem_b + STAGES * Cfg::kBStage;  // epilogue staging, 1024-aligned
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_out + 2 * Cfg::kOutTile);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_out + Cfg::kOutTiles * Cfg::kOutTile);
     uint64_t *full = bars;
     uint64_t *empty = bars + STAGES;
     uint64_t *tfull = bars + 2 * STAGES;
@@ -427,10 +433,14 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                     // completion barrier: own `full` (single CTA) or the leader's (pair)
                     const uint32_t fb = CG == 2 ? ptx::mapa(ptx::smem_u32(&full[stage]), 0)
                                                 : ptx::smem_u32(&full[stage]);
+                    // instrumentation: skip this operand's loads after the CTA's first tile
+                    const bool skip = IMCONV_INSTRUMENT && tile != tile_start &&
+                                      (p.dbg_flags & (is_a ? 2 : 1)) != 0;
                     if (mine) {
                         timed_wait_g(&empty[stage], phase ^ 1, w_empty);
                         if (rank == 0)
-                            ptx::mbar_arrive_expect_tx(&full[stage], CG * nsub * (is_a ? Cfg::kASub : Cfg::kBSub));
+                            ptx::mbar_arrive_expect_tx(&full[stage],
+                                                       skip ? 0u : CG * nsub * (is_a ? Cfg::kASub : Cfg::kBSub));
                     }
                     uint8_t *a_st = smem_a + stage * Cfg::kAStageK;
                     uint8_t *b_st = smem_b + stage * Cfg::kBStage;
@@ -438,15 +448,23 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         int brow;
                         if (p.tps == 1) {
                             const int c0 = kw.chunk * Cfg::kBKE;
-                            if (is_a && mine) {
-                                if constexpr (CG == 2)
+                            if (is_a && mine && !skip) {
+                                if (p.a_tiled) {
+                                    if constexpr (CG == 2)
+                                        ptx::tma_load_2d_2sm(a_st + u * Cfg::kASub, &tmap_a, fb, c0,
+                                                             static_cast<int>(m0), pol);
+                                    else
+                                        ptx::tma_load_2d(a_st + u * Cfg::kASub, &tmap_a, &full[stage], c0,
+                                                         static_cast<int>(m0), pol);
+                                } else if constexpr (CG == 2) {
                                     ptx::tma_load_im2col_4d_2sm(a_st + u * Cfg::kASub, &tmap_a, fb, c0, w0, h0, n0,
                                                                 static_cast<uint16_t>(kw.s * p.dw),
                                                                 static_cast<uint16_t>(kw.r * p.dh), pol);
-                                else
+                                } else {
                                     ptx::tma_load_im2col_4d(a_st + u * Cfg::kASub, &tmap_a, &full[stage], c0, w0, h0,
                                                             n0, static_cast<uint16_t>(kw.s * p.dw),
                                                             static_cast<uint16_t>(kw.r * p.dh), pol);
+                                }
                             }
                             brow = kw.tap * p.c + c0;
                             kw.next(p.order, p.r, p.s, p.c_chunks);
@@ -455,7 +473,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                             // reduction (the paper's multi-tile packing, §4.2); tap t
                             // occupies a (kRows x rb) block
                             const int tap0 = (kb * KSUB + u) * p.tps;
-                            if (is_a && mine) {
+                            if (is_a && mine && !skip) {
                                 for (int t = 0; t < p.tps; ++t) {
                                     const int tap = min(tap0 + t, p.rs - 1);  // past-the-end taps meet zero filter rows
                                     const int r = tap / p.s, s = tap - (tap / p.s) * p.s;
@@ -473,7 +491,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                             }
                             brow = tap0 * p.c;
                         }
-                        if (!is_a && mine) {
+                        if (!is_a && mine && !skip) {
                             uint8_t *b_dst = b_st + u * Cfg::kBSub;
                             if constexpr (CG == 2) {
                                 if (p.b_3d) {
@@ -610,13 +628,16 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             p.dbg[blockIdx.x * 8 + 4] = w_full;
         }
     } else if (warp >= 4 && warp < 8) {
-        // ===== epilogue: TMEM -> registers -> one swizzled 128-row tile -> ONE TMA store =====
-        // The SM's TMA unit costs ~200+ cycles per operation whatever its size
-        // (tools/tma_bench.cu), so the four epilogue warps stage a whole
-        // 128 x 128-byte tile and a single thread stores it.
+        // ===== epilogue: TMEM -> registers -> one swizzled 128-row tile per 128-byte column chunk =====
+        // The four warps stage a whole 128 x 128-byte tile (one TMA store: the
+        // SM's TMA unit costs ~200+ cycles per operation whatever its size,
+        // tools/tma_bench.cu) and hand it to the store warp, which issues the
+        // store -- a TMA issue blocks its thread ~400 cycles, which must not sit
+        // on the critical path of the warps draining TMEM.  Handshake per
+        // staging tile b (named barriers, 128 epilogue + 32 store threads):
+        // FULL(b) = staged, EMPTY(b) = the store that last read b has finished.
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32) = block rows
         const uint32_t row = quarter * 32 + lane;
-        const bool issuer = (warp == 4 && lane == 0);
         constexpr int kOC = Cfg::kOutCols;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -634,6 +655,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
 #pragma unroll 1
                 for (int j = 0; j < BN / kOC; ++j) {
                     const int col0 = n_tile * BN + j * kOC;
+                    if (col0 >= p.k || row0 >= p.m) continue;  // uniform (the store warp skips it too)
                     uint32_t v[kOC];
                     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                            static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC);
@@ -643,27 +665,21 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
                     ptx::tmem_ld_wait();
                     const long long e1 = IMCONV_INSTRUMENT ? clock64() : 0;
-                    if (col0 >= p.k || row0 >= p.m) continue;  // uniform over the 4 warps
-                    uint8_t *buf = smem_out + (chunk_ctr & 1) * Cfg::kOutTile;
-                    if (issuer) ptx::tma_store_wait_read<1>();  // the store issued 2 chunks ago has read buf
-                    ptx::named_bar_sync(1, 128);
+                    const uint32_t b = chunk_ctr & 1;
+                    if (chunk_ctr >= 2) ptx::named_bar_sync(3 + b, 160);  // EMPTY(b)
                     const long long e2 = IMCONV_INSTRUMENT ? clock64() : 0;
-                    stage_row128<OUT>(buf, row, v);
+                    stage_row128<OUT>(smem_out + b * Cfg::kOutTile, row, v);
                     ptx::fence_proxy_async_smem();
-                    const long long e3 = IMCONV_INSTRUMENT ? clock64() : 0;
-                    ptx::named_bar_sync(1, 128);
+                    ptx::named_bar_arrive(1 + b, 160);  // FULL(b)
                     if (IMCONV_INSTRUMENT) {
                         t_ld += e1 - e0;
-                        t_bar += (e2 - e1) + (clock64() - e3);
-                        t_st += e3 - e2;
-                    }
-                    if (issuer) {
-                        ptx::tma_store_2d(&tmap_y, buf, col0, static_cast<int>(row0));  // clipped at M / K
-                        ptx::tma_store_commit();
+                        t_bar += e2 - e1;
+                        t_st += clock64() - e2;
                     }
                     ++chunk_ctr;
                 }
             }
+            // every TMEM load of this accumulator has completed: release it
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -675,8 +691,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if (issuer) ptx::tma_store_wait<0>();
-        __syncwarp();
+        // the store warp frees the second-to-last tile after the last chunk: consume
+        // that arrival so no named barrier is left half-arrived at exit
+        if (chunk_ctr >= 2) ptx::named_bar_sync(3 + (chunk_ctr & 1), 160);
         if (IMCONV_INSTRUMENT && p.dbg && lane == 0 && quarter == 0) {
             p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 6] = w_tfull;
@@ -684,6 +701,34 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             p.dbg[148 * 8 + blockIdx.x * 4 + 0] = t_bar;
             p.dbg[148 * 8 + blockIdx.x * 4 + 1] = t_st;
         }
+    } else if (warp == 9) {
+        // ===== output store issuer: one TMA store per staged 128 x 128-byte tile =====
+        constexpr int kOC = Cfg::kOutCols;
+        uint32_t chunk_ctr = 0;
+        for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
+            const long long m_tile = tile / p.n_tiles;
+            const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
+            for (int mt = 0; mt < MT; ++mt) {
+                const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;
+                for (int j = 0; j < BN / kOC; ++j) {
+                    const int col0 = n_tile * BN + j * kOC;
+                    if (col0 >= p.k || row0 >= p.m) continue;
+                    const uint32_t b = chunk_ctr & 1;
+                    ptx::named_bar_sync(1 + b, 160);  // FULL(b)
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&tmap_y, smem_out + b * Cfg::kOutTile, col0,
+                                          static_cast<int>(row0));  // clipped at M / K
+                        ptx::tma_store_commit();
+                        ptx::tma_store_wait_read<1>();  // the previous chunk's store has read its tile
+                    }
+                    __syncwarp();
+                    if (chunk_ctr >= 1) ptx::named_bar_arrive(3 + (b ^ 1), 160);  // EMPTY(b ^ 1)
+                    ++chunk_ctr;
+                }
+            }
+        }
+        if (lane == 0) ptx::tma_store_wait<0>();
+        __syncwarp();
     }
 
     if constexpr (CG == 2) {

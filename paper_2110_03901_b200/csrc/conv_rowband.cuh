@@ -92,7 +92,7 @@ struct RowbandCfg {
 };
 
 template <int ELEM, int OUT, int BN, int TP, int NP>
-__global__ void __launch_bounds__(kThreadsGeneric, 1)
+__global__ void __launch_bounds__(kThreadsRowband, 1)
     conv_rowband_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_y,
                         const RowbandParams p) {
     using Cfg = RowbandCfg<ELEM, OUT, BN, TP>;

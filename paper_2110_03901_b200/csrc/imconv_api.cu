@@ -187,7 +187,7 @@ int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandPa
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid, kThreadsGeneric, smem, st>>>(tw, ty, p);
+    kern<<<grid, kThreadsRowband, smem, st>>>(tw, ty, p);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
@@ -258,7 +258,7 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
             break;
         }
     }
-    if (g_debug_flags >> 8) p.rps = std::min(rows_needed, g_debug_flags >> 8);  // experiment override
+    if ((g_debug_flags >> 8) & 0xff) p.rps = std::min(rows_needed, (g_debug_flags >> 8) & 0xff);  // experiment override
     p.a_stage_bytes = p.rps * p.row_bytes_planes;
     p.in_rows = (rows_needed + p.rps - 1) / p.rps * p.rps;
     // taps ordered by their run address inside a stage, paired neighbour-wise
@@ -467,7 +467,21 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     CUtensorMap ta, tb;
     std::memset(&ta, 0, sizeof(ta));
     std::memset(&tb, 0, sizeof(tb));
-    {
+    // 1x1, stride 1, no padding: the implicit im2col is the identity, so A is
+    // the (N*H*W, C) activation matrix itself -- a tiled map (one TMA box of
+    // 128 B of channels x 128*mt rows per k-subtile) replaces the im2col map.
+    const bool a_tiled = R == 1 && S == 1 && a->stride_h == 1 && a->stride_w == 1 && a->pad_h == 0 &&
+                         a->pad_w == 0 && row_bytes == 128 && !(g_debug_flags & 0x1000);
+    if (a_tiled) {
+        cuuint64_t gdim[2] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(N * H * W)};
+        cuuint64_t gstride[1] = {static_cast<cuuint64_t>(C * E)};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(row_bytes / E), static_cast<cuuint32_t>(kBM * mt)};
+        cuuint32_t estride[2] = {1, 1};
+        if (g_encode_tiled(&ta, tmap_dtype(a->in_dtype), 2, const_cast<void *>(a->x), gdim, gstride, box, estride,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, a_swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    } else {
         cuuint64_t gdim[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                               static_cast<cuuint64_t>(N)};
         cuuint64_t gstride[3] = {static_cast<cuuint64_t>(C * E), static_cast<cuuint64_t>(W * C * E),
@@ -567,6 +581,8 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     // bf16/fp16 C = 8 with KSUB = 1 and >= 4 stages (variants 0 and 2)
     p.a_gather = (row_bytes == 16 && E == 2 && !use_pair && variant != 1) ? 1 : 0;
     p.x = static_cast<const uint8_t *>(a->x);
+    p.a_tiled = a_tiled ? 1 : 0;
+    p.dbg_flags = g_debug_flags & 0xff;
 
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
@@ -591,11 +607,13 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     if (grid > tiles) grid = static_cast<int>(tiles);
     switch (a->in_dtype) {
         case IMCONV_BF16:
-            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
-                                              : dispatch_bn<ELEM_BF16, OUT_BF16>(bn, variant, ta, tb, ty, p, grid, st);
+            return a->out_dtype == IMCONV_F32
+                       ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
+                       : dispatch_bn<ELEM_BF16, OUT_BF16>(bn, variant, ta, tb, ty, p, grid, st);
         case IMCONV_F16:
-            return a->out_dtype == IMCONV_F32 ? dispatch_bn<ELEM_F16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
-                                              : dispatch_bn<ELEM_F16, OUT_F16>(bn, variant, ta, tb, ty, p, grid, st);
+            return a->out_dtype == IMCONV_F32
+                       ? dispatch_bn<ELEM_F16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
+                       : dispatch_bn<ELEM_F16, OUT_F16>(bn, variant, ta, tb, ty, p, grid, st);
         case IMCONV_I8: return dispatch_bn<ELEM_I8, OUT_I32>(bn, variant, ta, tb, ty, p, grid, st);
         default: return IMCONV_EDTYPE;
     }

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--waits", action="store_true", help="print per-role wait-cycle instrumentation")
     ap.add_argument("--dbg-flags", type=int, default=0, help="instrumentation: disable kernel roles (wrong results)")
     ap.add_argument("--rps", type=int, default=0, help="row-band kernel: input rows per stage override (0 = auto)")
+    ap.add_argument("--epi", type=int, default=0, help="generic kernel: epilogue groups override (1 or 2, 0 = auto)")
     args = ap.parse_args()
     if args.waits or args.dbg_flags:
         os.environ["IMCONV_INSTRUMENTED"] = "1"
@@ -45,7 +46,7 @@ def main():
         x = torch.randn((sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev).to(torch.bfloat16)
         w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev) * 0.05).to(torch.bfloat16)
     order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[args.order]
-    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8))
+    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8) | (args.epi << 16))
     def once():
         if args.explicit:
             low = K.im2col_nhwc(x, sp.h_f, sp.w_f, *sp.conv_args(), True)
