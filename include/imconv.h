@@ -58,6 +58,8 @@ extern "C" {
 #define IMCONV_FLAG_MT1 8         /* one 128-pixel m-tile per CTA (N<=128 default is two)  */
 #define IMCONV_FLAG_GATHER16 16   /* 16-byte pixels: generic kernel with cp.async tap gathers
                                      instead of the row-band (stride-phase plane) kernel     */
+#define IMCONV_FLAG_NO_HALO 32    /* 128-byte pixels, stride 1, resident filter: generic
+                                     per-tap kernel instead of the halo-tile kernel          */
 
 /*
  * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,

@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libimconv.so")
 LIB_INSTR = os.path.join(PKG, "libimconv_instr.so")  # same sources, -DIMCONV_INSTRUMENT=1 (tools only)
 SOURCES = [os.path.join(CSRC, f) for f in ("imconv_api.cu", "lru.cpp")]
-HEADERS = [os.path.join(CSRC, f) for f in ("ptx.cuh", "conv_kernel.cuh", "conv_rowband.cuh", "aux_kernels.cuh")] + [
+HEADERS = [os.path.join(CSRC, f) for f in ("ptx.cuh", "conv_kernel.cuh", "conv_rowband.cuh", "conv_halo.cuh", "aux_kernels.cuh")] + [
     os.path.join(ROOT, "include", "imconv.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1,0 +1,256 @@
+// conv_halo.cuh -- stride-1 convolutions whose pixel is exactly one 128-byte
+// swizzle row (bf16/fp16 C = 64, int8 C = 128) and whose whole filter fits in
+// shared memory (e.g. the ResNet-50 stage-2 3x3 layers).
+//
+// The generic kernel gathers every filter tap separately: one im2col TMA box
+// of 128 output pixels per tap, so each input pixel crosses the SM's shared
+// memory R*S times.  For these N = 64 layers shared-memory bandwidth (operand
+// writes + tensor-core reads), not the tensor core, is the bound.  Here a block
+// is TPR whole output rows of one image laid out with a padded row pitch
+// QP = Q + (S-1)*dw:
+//
+//   accumulator row m = p_rel * QP + q        (q >= Q: halo columns, discarded)
+//
+// and ONE 4-D TMA box loads the TR = TPR + (R-1)*dh input rows x QP pixels the
+// block needs (out-of-image rows / columns are zero-filled by the hardware:
+// the reference's virtual padding, lowering.py:59-64).  Input pixel
+// (p_rel + r*dh, q + s*dw) of that tile is smem row m + r*dh*QP + s*dw, so
+// filter tap <r,s> is the same tile read through a descriptor whose start
+// moves by that many 128-byte rows -- the tensor core applies the SW128
+// swizzle by absolute shared-memory address (tools/desc_probe.cu), so shifted
+// descriptors need no re-layout.  The paper's channel-first tap decomposition
+// (lowering.py:136-143) becomes descriptor arithmetic, and each input pixel
+// is written to shared memory once per block instead of once per tap.
+//
+// The filter (R*S taps x 128-byte k-rows x BN) stays resident.  Warp roles as
+// in conv_fwd_kernel: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator,
+// 4-7 = epilogue (TMEM -> swizzled staging of the TPR*Q valid pixels), 9 =
+// store issuer (one 4-D TMA store {128 B of channels, Q, TPR, 1} per chunk).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+#include "conv_kernel.cuh"
+#include "ptx.cuh"
+
+namespace imconv {
+
+struct HaloParams {
+    int n, h, w, k;
+    int r, s, ph, pw, dh, dw;
+    int p, q;
+    int qp;                 // padded row pitch of the tile (Q + (S-1)*dw)
+    int tpr;                // output rows per block (floor(128 / qp))
+    int tr;                 // input rows per block (tpr + (R-1)*dh)
+    int p_tiles;            // ceil(P / tpr)
+    long long tiles;        // n * p_tiles * n_tiles
+    int n_tiles;            // output-channel blocks of BN
+    int a_stage_bytes;      // tr * qp * 128 rounded up to 1024 (+ slack rows the last taps over-read)
+    int a_box_bytes;        // tr * qp * 128 (bytes the TMA delivers)
+    int n_stages;
+    int b_bytes;            // resident filter bytes (R*S taps)
+};
+
+template <int ELEM, int OUT, int BN>
+struct HaloCfg {
+    static constexpr int kE = ElemTraits<ELEM>::kBytes;
+    static constexpr int kBKE = kRowBytes / kE;           // k-rows (channels) per tap
+    static constexpr int kNC = kRowBytes / kE;            // columns per 128-byte B chunk
+    static constexpr int kBTap = BN * kRowBytes;          // resident B bytes per tap (BN/kNC chunks x kBKE rows x 128 B)
+    static constexpr int kBChunk = kBKE * kRowBytes;      // one column chunk of one tap
+    static constexpr int kMmaK = 32 / kE;
+    static constexpr int kMmaPerTap = kBKE / kMmaK;       // = 4
+    static constexpr int kTmemCols = 2 * BN;
+    static constexpr int kOutCols = (OUT == OUT_BF16 || OUT == OUT_F16) ? 64 : 32;
+    static constexpr int kOutTile = kBM * 128;
+    static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
+};
+
+template <int ELEM, int OUT, int BN>
+__global__ void __launch_bounds__(kThreadsGeneric, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                     const __grid_constant__ CUtensorMap tmap_y, const HaloParams p) {
+    using Cfg = HaloCfg<ELEM, OUT, BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *smem_b = smem;                                 // resident filter (1024-aligned size)
+    uint8_t *smem_out = smem_b + p.b_bytes;                 // 2 staging tiles
+    uint8_t *smem_a = smem_out + 2 * Cfg::kOutTile;         // input-tile ring
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_a + p.n_stages * p.a_stage_bytes);
+    uint64_t *full = bars;
+    uint64_t *empty = bars + p.n_stages;
+    uint64_t *tfull = bars + 2 * p.n_stages;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *bfull = tempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
+
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const uint32_t lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmap_a);
+        ptx::prefetch_tmap(&tmap_b);
+        ptx::prefetch_tmap(&tmap_y);
+        for (int i = 0; i < p.n_stages; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 4);
+        }
+        ptx::mbar_init(bfull, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int rs = p.r * p.s;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- resident filter: per tap, all BN/kNC column chunks in one 3-D box ----
+            const uint64_t pol_w = ptx::policy_evict_last();
+            ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(p.b_bytes));
+            const int nb0_chunks = 0;
+            (void)nb0_chunks;
+            // (the resident filter covers one BN-wide block of output channels: n_tiles == 1)
+            for (int t = 0; t < rs; ++t) ptx::tma_load_3d(smem_b + t * Cfg::kBTap, &tmap_b, bfull, 0, t * Cfg::kBKE, 0, pol_w);
+            // ---- input tiles: one 4-D box {128 B of channels, QP pixels, TR rows, 1 image} ----
+            const uint64_t pol_a = ptx::policy_evict_normal();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+                const int pt = static_cast<int>(tile % p.p_tiles);
+                const int n = static_cast<int>(tile / p.p_tiles);
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(p.a_box_bytes));
+                ptx::tma_load_4d(smem_a + stage * p.a_stage_bytes, &tmap_a, &full[stage], 0, -p.pw,
+                                 pt * p.tpr - p.ph, n, pol_a);
+                if (++stage == p.n_stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---- MMA issuer: R*S taps x kMmaPerTap MMAs per block, all operands warp-uniform ----
+        const uint32_t idesc = make_idesc<ELEM, BN>();
+        const uint32_t a_base = __shfl_sync(0xffffffffu, ptx::smem_u32(smem_a), 0);
+        const uint32_t b_base = __shfl_sync(0xffffffffu, ptx::smem_u32(smem_b), 0);
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
+        const uint64_t adesc0 = ptx::smem_desc(a_base, 16, 1024, ptx::LAYOUT_SW128);
+        const uint64_t bdesc0 = ptx::smem_desc(b_base, Cfg::kBChunk, 1024, ptx::LAYOUT_SW128);
+        ptx::mbar_wait(bfull, 0);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem_u + static_cast<uint32_t>(acc * BN);
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            const uint64_t a_st = adesc0 + static_cast<uint64_t>((stage * p.a_stage_bytes) >> 4);
+            for (int r = 0; r < p.r; ++r) {
+                for (int s = 0; s < p.s; ++s) {
+                    // tap <r,s>: the tile shifted by r*dh rows of QP pixels and s*dw pixels
+                    const uint64_t a_tap = a_st + static_cast<uint64_t>(((r * p.dh) * p.qp + s * p.dw) * 8);
+                    const uint64_t b_tap = bdesc0 + static_cast<uint64_t>(((r * p.s + s) * Cfg::kBTap) >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk) {
+                        const uint32_t accum = (r | s | kk) != 0 ? 1u : 0u;
+                        const uint64_t ad = a_tap + static_cast<uint64_t>(kk * 2);  // +32 bytes along K
+                        const uint64_t bd = b_tap + static_cast<uint64_t>((kk * Cfg::kMmaK * kRowBytes) >> 4);
+                        if constexpr (ELEM == ELEM_I8)
+                            ptx::mma_i8_elect(d, ad, bd, idesc, accum);
+                        else
+                            ptx::mma_f16_elect(d, ad, bd, idesc, accum);
+                    }
+                }
+            }
+            ptx::mma_commit_elect(&empty[stage]);
+            ptx::mma_commit_elect(&tfull[acc]);
+            if (++stage == p.n_stages) {
+                stage = 0;
+                phase ^= 1;
+            }
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---- epilogue: TMEM row m = p_rel*QP + q -> staging row p_rel*Q + q (halo columns dropped) ----
+        const int quarter = warp & 3;
+        const int m = quarter * 32 + static_cast<int>(lane);
+        const int p_rel = m / p.qp;
+        const int qq = m - p_rel * p.qp;
+        const bool valid = qq < p.q && p_rel < p.tpr;
+        const uint32_t srow = static_cast<uint32_t>(p_rel * p.q + qq);
+        constexpr int kOC = Cfg::kOutCols;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        uint32_t chunk_ctr = 0;
+        for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int j = 0; j < BN / kOC; ++j) {
+                if (j * kOC >= p.k) continue;  // uniform (the store warp skips it too)
+                uint32_t v[kOC];
+                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                       static_cast<uint32_t>(acc * BN + j * kOC);
+#pragma unroll
+                for (int hh = 0; hh < kOC / 32; ++hh)
+                    ptx::tmem_ld_32x32b_x32(taddr + hh * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * hh));
+                ptx::tmem_ld_wait();
+                const uint32_t b = chunk_ctr & 1;
+                if (chunk_ctr >= 2) ptx::named_bar_sync(3 + b, 160);  // EMPTY(b)
+                if (valid) stage_row128<OUT>(smem_out + b * Cfg::kOutTile, srow, v);
+                ptx::fence_proxy_async_smem();
+                ptx::named_bar_arrive(1 + b, 160);  // FULL(b)
+                ++chunk_ctr;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+        if (chunk_ctr >= 2) ptx::named_bar_sync(3 + (chunk_ctr & 1), 160);
+    } else if (warp == 9) {
+        // ---- store issuer: one 4-D box {128 B of channels, Q, TPR rows, 1} per staged chunk ----
+        constexpr int kOC = Cfg::kOutCols;
+        uint32_t chunk_ctr = 0;
+        for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            const int pt = static_cast<int>(tile % p.p_tiles);
+            const int n = static_cast<int>(tile / p.p_tiles);
+            for (int j = 0; j < BN / kOC; ++j) {
+                if (j * kOC >= p.k) continue;
+                const uint32_t b = chunk_ctr & 1;
+                ptx::named_bar_sync(1 + b, 160);  // FULL(b)
+                if (lane == 0) {
+                    ptx::tma_store_4d(&tmap_y, smem_out + b * Cfg::kOutTile, j * kOC, 0, pt * p.tpr, n);  // clipped at P
+                    ptx::tma_store_commit();
+                    ptx::tma_store_wait_read<1>();
+                }
+                __syncwarp();
+                if (chunk_ctr >= 1) ptx::named_bar_arrive(3 + (b ^ 1), 160);  // EMPTY(b ^ 1)
+                ++chunk_ctr;
+            }
+        }
+        if (lane == 0) ptx::tma_store_wait<0>();
+        __syncwarp();
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    }
+}
+
+}  // namespace imconv

@@ -18,6 +18,7 @@
 #include "../../include/imconv.h"
 #include "aux_kernels.cuh"
 #include "conv_kernel.cuh"
+#include "conv_halo.cuh"
 #include "conv_rowband.cuh"
 
 namespace imconv {
@@ -194,6 +195,136 @@ int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandPa
 }
 
 constexpr int kNotApplicable = -1000;  // internal: layer does not qualify for a specialised path
+
+template <int ELEM, int OUT, int BN>
+int launch_halo(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const HaloParams &p, int smem,
+                int grid, cudaStream_t st) {
+    auto kern = conv_halo_kernel<ELEM, OUT, BN>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    });
+    if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
+    kern<<<grid, kThreadsGeneric, smem, st>>>(ta, tb, ty, p);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+// Halo-tile path (conv_halo.cuh): stride 1, one 128-byte swizzle row per pixel
+// (bf16/fp16 C = 64, int8 C = 128), K = BN in {64,128,256} with the whole
+// filter resident in shared memory.  Returns kNotApplicable otherwise.
+int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st) {
+    const int E = elem_bytes(a->in_dtype);
+    if (a->c * E != 128 || a->stride_h != 1 || a->stride_w != 1) return kNotApplicable;
+    if (a->tile_n != 0 || a->order == IMCONV_ORDER_FILTER_MAJOR) return kNotApplicable;
+    const int K = static_cast<int>(a->k), R = static_cast<int>(a->r), S = static_cast<int>(a->s);
+    const int nc = 128 / E;
+    // 1x1 filters have no tap reuse to gain, and the padded row pitch costs M utilisation
+    if (R * S == 1) return kNotApplicable;
+    if (K % nc != 0 || !(K == 64 || K == 128 || K == 256) || (E == 1 && K < 128)) return kNotApplicable;
+    HaloParams p{};
+    p.n = static_cast<int>(a->n);
+    p.h = static_cast<int>(a->h);
+    p.w = static_cast<int>(a->w_);
+    p.k = K;
+    p.r = R;
+    p.s = S;
+    p.ph = a->pad_h;
+    p.pw = a->pad_w;
+    p.dh = a->dil_h;
+    p.dw = a->dil_w;
+    p.p = static_cast<int>(P);
+    p.q = static_cast<int>(Q);
+    p.qp = static_cast<int>(Q) + (S - 1) * p.dw;
+    if (p.qp > 128 || p.qp > 256) return kNotApplicable;
+    p.tpr = 128 / p.qp;
+    p.tr = p.tpr + (R - 1) * p.dh;
+    if (p.tr > 256) return kNotApplicable;
+    p.p_tiles = static_cast<int>((P + p.tpr - 1) / p.tpr);
+    p.n_tiles = 1;
+    p.tiles = static_cast<long long>(p.n) * p.p_tiles;
+    p.a_box_bytes = p.tr * p.qp * 128;
+    // the last taps read up to 128 + (R-1)*dh*QP + (S-1)*dw rows (rows past the box feed only discarded accumulator rows)
+    const int rows_read = std::max(p.tr * p.qp, 128 + (R - 1) * p.dh * p.qp + (S - 1) * p.dw);
+    p.a_stage_bytes = (rows_read * 128 + 1023) / 1024 * 1024;
+    p.b_bytes = R * S * K * 128;
+    const int kOutTiles = 2 * kBM * 128;
+    const int fixed = p.b_bytes + kOutTiles + 1024 /*align*/ + 1024 /*barriers*/;
+    if (p.b_bytes > 120 * 1024) return kNotApplicable;
+    p.n_stages = std::min(8, (kMaxDynSmem - fixed) / p.a_stage_bytes);
+    if (p.n_stages < 2) return kNotApplicable;
+    const int smem = fixed + p.n_stages * p.a_stage_bytes;
+
+    CUtensorMap ta, tb, ty;
+    std::memset(&ta, 0, sizeof(ta));
+    std::memset(&tb, 0, sizeof(tb));
+    std::memset(&ty, 0, sizeof(ty));
+    const int64_t N = a->n, H = a->h, W = a->w_, C = a->c;
+    {
+        cuuint64_t gdim[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(N)};
+        cuuint64_t gstride[3] = {static_cast<cuuint64_t>(C * E), static_cast<cuuint64_t>(W * C * E),
+                                 static_cast<cuuint64_t>(H * W * C * E)};
+        cuuint32_t box[4] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(p.qp),
+                             static_cast<cuuint32_t>(p.tr), 1};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (g_encode_tiled(&ta, tmap_dtype(a->in_dtype), 4, const_cast<void *>(a->x), gdim, gstride, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    {
+        cuuint64_t gdim[3] = {static_cast<cuuint64_t>(nc), static_cast<cuuint64_t>(R * S * C),
+                              static_cast<cuuint64_t>(K / nc)};
+        cuuint64_t gstride[2] = {static_cast<cuuint64_t>(K * E), static_cast<cuuint64_t>(nc * E)};
+        cuuint32_t box[3] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(K / nc)};
+        cuuint32_t es[3] = {1, 1, 1};
+        if (g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 3, const_cast<void *>(a->w), gdim, gstride, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    const int eo = (a->out_dtype == IMCONV_F32 || a->out_dtype == IMCONV_I32) ? 4 : 2;
+    {
+        CUtensorMapDataType dt = a->out_dtype == IMCONV_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : a->out_dtype == IMCONV_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                 : a->out_dtype == IMCONV_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        cuuint64_t gdim[4] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(P),
+                              static_cast<cuuint64_t>(N)};
+        cuuint64_t gstride[3] = {static_cast<cuuint64_t>(K * eo), static_cast<cuuint64_t>(Q * K * eo),
+                                 static_cast<cuuint64_t>(P * Q * K * eo)};
+        cuuint32_t box[4] = {static_cast<cuuint32_t>(128 / eo), static_cast<cuuint32_t>(Q),
+                             static_cast<cuuint32_t>(p.tpr), 1};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (g_encode_tiled(&ty, dt, 4, a->y, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    int grid = a->num_ctas > 0 ? a->num_ctas : sms;
+    if (grid > p.tiles) grid = static_cast<int>(p.tiles);
+#define IMCONV_HALO(EL, OUTK)                                                             \
+    switch (K) {                                                                          \
+        case 64: return launch_halo<EL, OUTK, 64>(ta, tb, ty, p, smem, grid, st);         \
+        case 128: return launch_halo<EL, OUTK, 128>(ta, tb, ty, p, smem, grid, st);       \
+        default: return launch_halo<EL, OUTK, 256>(ta, tb, ty, p, smem, grid, st);        \
+    }
+    const bool f32 = a->out_dtype == IMCONV_F32;
+    switch (a->in_dtype) {
+        case IMCONV_BF16:
+            if (f32) { IMCONV_HALO(ELEM_BF16, OUT_F32) } else { IMCONV_HALO(ELEM_BF16, OUT_BF16) }
+        case IMCONV_F16:
+            if (f32) { IMCONV_HALO(ELEM_F16, OUT_F32) } else { IMCONV_HALO(ELEM_F16, OUT_F16) }
+        case IMCONV_I8:
+            if (K == 128) return launch_halo<ELEM_I8, OUT_I32, 128>(ta, tb, ty, p, smem, grid, st);
+            return launch_halo<ELEM_I8, OUT_I32, 256>(ta, tb, ty, p, smem, grid, st);
+        default: return kNotApplicable;
+    }
+#undef IMCONV_HALO
+}
 
 // Row-band path for 16-byte pixels (bf16/fp16, C = 8).  Returns kNotApplicable
 // when the layer does not qualify (the caller then uses the generic kernel).
@@ -424,6 +555,13 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     if (!(a->flags & IMCONV_FLAG_GATHER16) && a->order != IMCONV_ORDER_FILTER_MAJOR) {
         const int rb = try_rowband(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
         if (rb != kNotApplicable) return rb;
+    }
+
+    // 128-byte pixels, stride 1, filter resident in smem: halo tiles (each
+    // input pixel enters shared memory once per block, taps are descriptor offsets)
+    if (!(a->flags & IMCONV_FLAG_NO_HALO)) {
+        const int hr = try_halo(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
+        if (hr != kNotApplicable) return hr;
     }
 
     const int bn = pick_bn(a->in_dtype, K, a->tile_n);

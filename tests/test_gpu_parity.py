@@ -96,6 +96,49 @@ def test_block_shape_and_grid_invariance(rng, tile_n, flags):
             assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), (c, ctas)
 
 
+# (N, H, W, R, S, K, pad_h, pad_w, dil_h, dil_w): halo-tile kernel shapes (stride 1,
+# 128-byte pixels) -- partial last row tile, dilation, non-square filters, wide K,
+# rows wider than half a tile (TPR = 1), and the ResNet stage-2 geometry.
+HALO_SHAPES = [
+    (2, 13, 11, 3, 3, 64, 1, 1, 1, 1),
+    (3, 9, 17, 3, 3, 128, 2, 2, 2, 2),
+    (2, 12, 10, 5, 5, 64, 2, 2, 1, 1),
+    (2, 7, 21, 1, 3, 256, 0, 1, 1, 1),
+    (1, 6, 100, 3, 3, 64, 1, 1, 1, 1),
+    (2, 56, 56, 3, 3, 64, 1, 1, 1, 1),
+    (2, 10, 9, 3, 3, 64, 0, 0, 1, 1),
+]
+
+
+@pytest.mark.parametrize("shape", HALO_SHAPES)
+def test_halo_tiles_exact(rng, shape):
+    """bf16 C = 64 (and int8 C = 128) stride-1 layers run on conv_halo_kernel:
+    bit-exact against the oracle and identical to the per-tap generic kernel."""
+    P = _P()
+    from oracle import oracle as O
+    n, h, w_, r, s, k, ph, pw, dh, dw = shape
+    args = (1, 1, ph, pw, dh, dw)
+    x = rng.integers(-4, 5, size=(n, h, w_, 64)).astype(np.int64)
+    w = rng.integers(-4, 5, size=(r, s, 64, k)).astype(np.int64)
+    want = O.conv2d_nhwc_i64(x, w, *args)
+    xb = torch.from_numpy(x).float().cuda().bfloat16()
+    wb = torch.from_numpy(w).float().cuda().bfloat16()
+    launches0 = P._lib.lib.imconv_launch_count()
+    y = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    assert P._lib.lib.imconv_launch_count() == launches0 + 1
+    assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), shape
+    y_generic = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32, flags=P._lib.FLAG_NO_HALO)
+    assert torch.equal(y, y_generic)
+    # bf16 output (16-bit staging layout) vs the fp32 result rounded once
+    yb = P._kernels.conv2d_nhwc(xb, wb, *args)
+    assert torch.equal(yb, y.bfloat16())
+    if k >= 128:  # int8 needs C = 128 for a 128-byte pixel
+        xi = rng.integers(-128, 128, size=(n, h, w_, 128)).astype(np.int8)
+        wi = rng.integers(-128, 128, size=(r, s, 128, k)).astype(np.int8)
+        yi = P._kernels.conv2d_nhwc(torch.from_numpy(xi).cuda(), torch.from_numpy(wi).cuda(), *args)
+        assert np.array_equal(yi.cpu().numpy(), O.conv2d_nhwc_exact_f64(xi, wi, *args)), shape
+
+
 @pytest.mark.parametrize("order", ["reuse_aware", "filter_major"])
 def test_subtile_orders_identical(rng, order):
     P = _P()
