@@ -47,7 +47,7 @@ def committed_traffic(config: str):
     import glob
     if config != "cfg4":
         return None, None
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "launches_*.csv")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "launches_*.csv")))  # newest round / letter last
     for path in reversed(files):
         try:
             rows = [r for r in csv.reader(open(path)) if len(r) > 10]

@@ -171,10 +171,12 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
         int n_ent = 0;
 #pragma unroll
         for (int u = 0; u < kMaxEntPerThread; ++u) {
+            // entry k = input column col0 + k (consecutive lanes read consecutive
+            // pixels: whole 128-byte lines) -> plane k % sw, slot k / sw
             const int k = t + u * kProducers;
-            const int e = k / p.needed, j = k - (k / p.needed) * p.needed;
+            const int j = k / p.sw, e = k - j * p.sw;
             e_dst[u] = static_cast<uint32_t>(e * p.plane_bytes + j * 16);
-            e_col[u] = p.sw * j + e;
+            e_col[u] = k;
             n_ent += k < entries ? 1 : 0;
         }
         const size_t row_bytes = static_cast<size_t>(p.w) * 16;

@@ -103,6 +103,21 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *m, uin
         : "memory");
 }
 
+// L2 prefetches through a tensor map (no shared memory, no completion): warm L2
+// ahead of the shared-memory ring for operands that stream from DRAM.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *m, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_im2col_4d(const CUtensorMap *m, int32_t c, int32_t w, int32_t h, int32_t n,
+                                                       uint16_t off_w, uint16_t off_h) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.im2col [%0, {%1, %2, %3, %4}], {%5, %6};" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
+                 : "memory");
+}
+
 // 4-D im2col load over an NHWC tensor: base pixel {c, w, h, n} (w/h may be
 // negative: virtual padding), per-tap offsets {off_w, off_h} (= s*dw, r*dh).
 __device__ __forceinline__ void tma_load_im2col_4d(void *dst, const CUtensorMap *m, uint64_t *bar,

@@ -22,8 +22,8 @@ def main():
     ap.add_argument("--explicit", action="store_true", help="K3 im2col + K4 GEMM instead of the implicit kernel")
     ap.add_argument("--waits", action="store_true", help="print per-role wait-cycle instrumentation")
     ap.add_argument("--dbg-flags", type=int, default=0, help="instrumentation: disable kernel roles (wrong results)")
+    ap.add_argument("--once", action="store_true", help="one launch, no timing (for ncu --set full)")
     ap.add_argument("--rps", type=int, default=0, help="row-band kernel: input rows per stage override (0 = auto)")
-    ap.add_argument("--epi", type=int, default=0, help="generic kernel: epilogue groups override (1 or 2, 0 = auto)")
     args = ap.parse_args()
     if args.waits or args.dbg_flags:
         os.environ["IMCONV_INSTRUMENTED"] = "1"
@@ -35,7 +35,16 @@ def main():
     import paper_2110_03901_b200._kernels as K
 
     layers = {l.name: l for cfg in baseline_configs().values() for l in cfg}
-    layer = layers[args.layer]
+    for name in args.layer.split(","):  # several layers: one process (one ncu run covers them all)
+        run_one(args, layers[name])
+
+
+def run_one(args, layer):
+    import torch
+    from paper_2110_03901_b200 import _lib
+    from paper_2110_03901_b200._kernels import conv_device, gemm_device
+    import paper_2110_03901_b200._kernels as K
+
     sp = layer.spec if args.n is None else layer.spec.with_batch(args.n)
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
@@ -46,7 +55,7 @@ def main():
         x = torch.randn((sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev).to(torch.bfloat16)
         w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev) * 0.05).to(torch.bfloat16)
     order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[args.order]
-    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8) | (args.epi << 16))
+    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8))
     def once():
         if args.explicit:
             low = K.im2col_nhwc(x, sp.h_f, sp.w_f, *sp.conv_args(), True)
@@ -56,6 +65,9 @@ def main():
 
     once()
     torch.cuda.synchronize()
+    if args.once:
+        print(f"{layer.name}: launched once")
+        return
     # the timed launches are replayed from a CUDA graph so host-side launch
     # latency (ctypes + tensor-map encoding) cannot starve short kernels
     s = torch.cuda.Stream()
@@ -71,7 +83,7 @@ def main():
     ev[1].record()
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1]) / args.reps
-    print(f"{args.layer} n={sp.n}: {ms:.4f} ms  {sp.flops / ms / 1e9:.1f} TFLOP/s")
+    print(f"{layer.name} n={sp.n}: {ms:.4f} ms  {sp.flops / ms / 1e9:.1f} TFLOP/s")
     if args.waits:
         dbg = torch.zeros(148 * 12, dtype=torch.int64, device=dev)
         _lib.lib.imconv_debug_set_buffer(dbg.data_ptr())
