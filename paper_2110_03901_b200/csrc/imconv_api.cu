@@ -725,6 +725,18 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // B-stationary (1x1 layers with C*e <= 512 B): every k-subtile of a block fits the
+    // 4-deep B ring, so a CTA that always works on the same output-channel block loads
+    // its filter slice once.  Needs grid % n_tiles == 0 (persistent round-robin over
+    // n-fastest tiles then keeps each CTA on one n-block); allowed to drop <= 4% of SMs.
+    if (!use_pair && variant != 1 && !p.a_gather && p.k_stages <= 4 && !(g_debug_flags & 0x2000)) {
+        int g = static_cast<int>(std::min<long long>(grid, tiles));
+        g = g / p.n_tiles * p.n_tiles;
+        if (g >= p.n_tiles && g * 100 >= 96 * std::min<long long>(grid, tiles)) {
+            grid = g;
+            p.b_resident = 1;
+        }
+    }
 
     if (use_pair) {
         int g2 = grid;
