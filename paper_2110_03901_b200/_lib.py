@@ -90,6 +90,9 @@ def _load():
 
 
 lib = _load()
+# experiment switches (A/B measurements only): host-side debug flags of the C ABI
+if os.environ.get("IMCONV_DEBUG_FLAGS"):
+    lib.imconv_debug_set_flags(int(os.environ["IMCONV_DEBUG_FLAGS"], 0))
 
 
 def strerror(code: int) -> str:

@@ -107,6 +107,10 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: setup above overlaps the previous kernel's tail; no global memory is
+    // touched before every prerequisite grid has completed
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
     const int rs = p.r * p.s;
 
     if (warp == 0) {
@@ -114,9 +118,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             // ---- resident filter: per tap, all BN/kNC column chunks in one 3-D box ----
             const uint64_t pol_w = ptx::policy_evict_last();
             ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(p.b_bytes));
-            const int nb0_chunks = 0;
-            (void)nb0_chunks;
-            // (the resident filter covers one BN-wide block of output channels: n_tiles == 1)
+            // (the resident filter covers all K = BN output channels: n_tiles == 1)
             for (int t = 0; t < rs; ++t) ptx::tma_load_3d(smem_b + t * Cfg::kBTap, &tmap_b, bfull, 0, t * Cfg::kBKE, 0, pol_w);
             // ---- input tiles: one 4-D box {128 B of channels, QP pixels, TR rows, 1 image} ----
             const uint64_t pol_a = ptx::policy_evict_normal();

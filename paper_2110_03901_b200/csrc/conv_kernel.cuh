@@ -331,6 +331,10 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: setup above overlaps the previous kernel's tail; no global memory is
+    // touched before every prerequisite grid has completed
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
 
     if (CG == 1 && STAGES >= 4 && p.a_gather && (warp == 0 || warp == 2)) {  // (>= 2 ring slots per gather warp)
         // ===== A producers for 16-byte pixels (bf16 C = 8: the ResNet stem) =====

@@ -136,6 +136,10 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: setup above overlaps the previous kernel's tail; no global memory is
+    // touched before every prerequisite grid has completed
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
 
     if (warp == 0) {
         if (lane == 0) {

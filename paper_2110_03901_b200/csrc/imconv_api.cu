@@ -27,6 +27,11 @@ namespace {
 thread_local int64_t g_launches = 0;
 long long *g_debug_buf = nullptr;  // instrumentation target (imconv_debug_set_buffer)
 int g_debug_flags = 0;
+// imconv_debug_set_flags layout: bits 0-7 kernel instrumentation switches (instrumented
+// build), bits 8-15 row-band rows-per-stage override, bits 16+ host-side A/B switches
+constexpr int kDbgNoTiledA = 1 << 16;     // 1x1 stride-1 layers keep the im2col A map
+constexpr int kDbgNoBResident = 1 << 17;  // never load the filter slice once per CTA
+constexpr int kDbgNoPdl = 1 << 18;        // launch without programmatic stream serialization
 
 std::mutex g_mu;
 PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
@@ -83,6 +88,37 @@ CUtensorMapDataType tmap_dtype(int in_dtype) {
 
 int elem_bytes(int in_dtype) { return in_dtype == IMCONV_I8 ? 1 : 2; }
 
+// Conv kernels are launched with programmatic stream serialization (PDL): the
+// next kernel's CTAs may start their setup (barrier init, TMEM allocation,
+// tensor-map prefetch) on SMs this kernel has released, and block in
+// griddepcontrol.wait before touching global memory.  Debug flag kDbgNoPdl turns
+// it off (A/B measurements).
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kern, int grid, int block, int smem, cudaStream_t st, int cluster, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(block));
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (!(g_debug_flags & kDbgNoPdl)) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = static_cast<unsigned>(cluster);
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = static_cast<unsigned>(na);
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int ELEM, int OUT, int BN, int STAGES, int KSUB, int MT, int CG = 1>
 int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const ConvParams &p, int grid,
                 cudaStream_t st) {
@@ -96,24 +132,9 @@ int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap 
             attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    if constexpr (CG == 1) {
-        kern<<<grid, kThreadsGeneric, Cfg::kSmemBytes, st>>>(ta, tb, ty, p);
-    } else {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
-        cfg.blockDim = dim3(kThreadsGeneric);
-        cfg.dynamicSmemBytes = Cfg::kSmemBytes;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta, tb, ty, p);
-        if (le != cudaSuccess) return static_cast<int>(le);
-    }
+    const int g = CG == 1 ? grid : (grid & ~1);
+    cudaError_t le = launch_pdl(kern, g, kThreadsGeneric, Cfg::kSmemBytes, st, CG, ta, tb, ty, p);
+    if (le != cudaSuccess) return static_cast<int>(le);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
@@ -188,7 +209,8 @@ int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandPa
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid, kThreadsRowband, smem, st>>>(tw, ty, p);
+    cudaError_t le = launch_pdl(kern, grid, kThreadsRowband, smem, st, 1, tw, ty, p);
+    if (le != cudaSuccess) return static_cast<int>(le);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
@@ -206,7 +228,8 @@ int launch_halo(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap 
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     });
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    kern<<<grid, kThreadsGeneric, smem, st>>>(ta, tb, ty, p);
+    cudaError_t le = launch_pdl(kern, grid, kThreadsGeneric, smem, st, 1, ta, tb, ty, p);
+    if (le != cudaSuccess) return static_cast<int>(le);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
@@ -609,7 +632,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     // the (N*H*W, C) activation matrix itself -- a tiled map (one TMA box of
     // 128 B of channels x 128*mt rows per k-subtile) replaces the im2col map.
     const bool a_tiled = R == 1 && S == 1 && a->stride_h == 1 && a->stride_w == 1 && a->pad_h == 0 &&
-                         a->pad_w == 0 && row_bytes == 128 && !(g_debug_flags & 0x1000);
+                         a->pad_w == 0 && row_bytes == 128 && !(g_debug_flags & kDbgNoTiledA);
     if (a_tiled) {
         cuuint64_t gdim[2] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(N * H * W)};
         cuuint64_t gstride[1] = {static_cast<cuuint64_t>(C * E)};
@@ -729,7 +752,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     // 4-deep B ring, so a CTA that always works on the same output-channel block loads
     // its filter slice once.  Needs grid % n_tiles == 0 (persistent round-robin over
     // n-fastest tiles then keeps each CTA on one n-block); allowed to drop <= 4% of SMs.
-    if (!use_pair && variant != 1 && !p.a_gather && p.k_stages <= 4 && !(g_debug_flags & 0x2000)) {
+    if (!use_pair && variant != 1 && !p.a_gather && p.k_stages <= 4 && !(g_debug_flags & kDbgNoBResident)) {
         int g = static_cast<int>(std::min<long long>(grid, tiles));
         g = g / p.n_tiles * p.n_tiles;
         if (g >= p.n_tiles && g * 100 >= 96 * std::min<long long>(grid, tiles)) {

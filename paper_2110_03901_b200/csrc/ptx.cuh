@@ -103,6 +103,15 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *m, uin
         : "memory");
 }
 
+// Programmatic dependent launch (PDL).  launch_dependents lets the next kernel
+// in the stream start its CTAs (setup only) as SMs free up; wait blocks until
+// every prerequisite grid has completed and its memory is visible.  Both are
+// no-ops for a launch without the programmatic-serialization attribute.
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // L2 prefetches through a tensor map (no shared memory, no completion): warm L2
 // ahead of the shared-memory ring for operands that stream from DRAM.
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *m, int32_t c0, int32_t c1) {
