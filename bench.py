@@ -418,12 +418,11 @@ def main(argv=None):
             d2h += hy.numel() * hy.element_size()
 
         def e2e_step():
+            # the public API with pinned HOST tensors: upload, conv and download
+            # of each layer (the pipelined host path of _kernels.conv2d_nhwc)
             for layer, sp, x, w, y in work:
                 hx, hw, hy = host[(sp, layer.dtype)]
-                xd = hx.to(dev, non_blocking=True)
-                wd = hw.to(dev, non_blocking=True)
-                yd = P._kernels.conv2d_nhwc(xd, wd, *sp.conv_args())
-                hy.copy_(yd, non_blocking=True)
+                P._kernels.conv2d_nhwc(hx, hw, *sp.conv_args(), out=hy)
 
         e2e_step()
         torch.cuda.synchronize()

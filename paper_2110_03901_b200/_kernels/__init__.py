@@ -47,7 +47,7 @@ def _plan_dtypes(x, w, compute, out_dtype):
     if D.is_integer_dtype(xd) and D.is_integer_dtype(wd):
         if compute not in (None, "int8"):
             raise ValueError(f"integer operands compute as int8, not {compute!r}")
-        np_res = None if (D.is_device_array(x) and xd == torch.int8) else np.int64
+        np_res = None if isinstance(x, torch.Tensor) else np.int64
         return torch.int8, torch.int32, np_res
     if compute is None:
         compute = "f16" if (xd == torch.float16 and wd == torch.float16) else "bf16"
@@ -64,7 +64,7 @@ def _plan_dtypes(x, w, compute, out_dtype):
     if odt not in (cdt, torch.float32):
         raise ValueError(f"output dtype {odt} not supported for {cdt} inputs")
     np_res = None
-    if not D.is_device_array(x):
+    if not isinstance(x, torch.Tensor):  # numpy in -> numpy out
         np_res = np.float64 if np.asarray(x).dtype == np.float64 or np.asarray(w).dtype == np.float64 \
             else np.float32
     return cdt, odt, np_res
@@ -131,16 +131,99 @@ def conv_device(xd: torch.Tensor, wd: torch.Tensor, sh=1, sw=1, ph=0, pw=0, dh=1
     return yk
 
 
+_COPY_STREAMS: dict = {}
+
+
+def _copy_streams(dev: torch.device):
+    """(host->device, device->host) copy streams of a device, created once."""
+    key = dev.index
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _COPY_STREAMS[key]
+
+
+def _conv_host(x: torch.Tensor, w: torch.Tensor, args, cdt, odt, out, **kw) -> torch.Tensor:
+    """Host tensors in, host tensor out, with the transfers pipelined.
+
+    The batch is split into up to four chunks: chunk i+1 is uploaded on a
+    copy stream while chunk i computes on the caller's current stream and
+    chunk i-1 is downloaded on a second copy stream, so the two PCIe
+    directions and the tensor cores overlap (a serial upload -> conv ->
+    download pays them one after another); uploads wait for no GPU work, so
+    consecutive calls overlap too.  The result is ordered before later work
+    on the caller's stream.  With ``out`` (pinned CPU tensor) the call
+    is asynchronous like a CUDA copy; without it, a pinned result is
+    allocated and the call returns once it is ready.
+    """
+    dev = D.require_cuda()
+    if cdt == torch.int8 and x.dtype != torch.int8:
+        _check_int8(x, "input")
+        x = x.to(torch.int8)
+    if cdt == torch.int8 and w.dtype != torch.int8:
+        _check_int8(w, "filter")
+        w = w.to(torch.int8)
+    x, w = x.contiguous(), w.contiguous()
+    n, h, wi, c = x.shape
+    r, s_, _, k = w.shape
+    sh, sw, ph, pw, dh, dw = args
+    shape = (n, _out_extent(h, r, sh, ph, dh), _out_extent(wi, s_, sw, pw, dw), k)
+    sync = out is None
+    if out is None:
+        out = torch.empty(shape, dtype=odt, pin_memory=True)
+    elif out.is_cuda or tuple(out.shape) != shape or out.dtype != odt or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous CPU tensor {shape} of {odt}")
+    cur = torch.cuda.current_stream(dev)
+    s_in, s_out = _copy_streams(dev)
+    # uploads read host memory into fresh device buffers, so they wait for no GPU
+    # work: the next call's upload overlaps this call's download (full-duplex PCIe)
+    chunks = max(1, min(4, n, x.numel() * x.element_size() // (8 << 20)))  # >= 8 MB per chunk
+    bounds = [(i * n // chunks, (i + 1) * n // chunks) for i in range(chunks)]
+    with torch.cuda.stream(s_in):
+        wd = w.to(dev, non_blocking=True)
+        wd = wd if wd.dtype == cdt else wd.to(cdt)
+    for a, b in bounds:
+        with torch.cuda.stream(s_in):
+            xd = x[a:b].to(dev, non_blocking=True)
+            xd = xd if xd.dtype == cdt else xd.to(cdt)
+            landed = torch.cuda.Event()
+            landed.record(s_in)
+        cur.wait_event(landed)
+        xd.record_stream(cur)
+        wd.record_stream(cur)
+        y = conv_device(xd, wd, *args, out_dtype=odt, **kw)
+        done = torch.cuda.Event()
+        done.record(cur)
+        s_out.wait_event(done)
+        with torch.cuda.stream(s_out):
+            out[a:b].copy_(y, non_blocking=True)
+        y.record_stream(s_out)
+    fin = torch.cuda.Event()
+    fin.record(s_out)
+    cur.wait_event(fin)
+    if sync:
+        cur.synchronize()
+    return out
+
+
 def conv2d_nhwc(x, w, sh, sw, ph, pw, dh, dw, *, compute: str | None = None, out_dtype=None,
-                tile_n: int = 0, num_ctas: int = 0, order: str = "reuse_aware", flags: int = 0):
+                tile_n: int = 0, num_ctas: int = 0, order: str = "reuse_aware", flags: int = 0, out=None):
     """Direct convolution NHWC x HWCN -> NHWC with virtual zero padding.
 
     Drop-in for the reference's ``conv2d_nhwc(x, w, sh, sw, ph, pw, dh, dw)``
     (_kernels/__init__.py:37-46).  Computed by the sm_100a implicit-im2col
-    tcgen05 kernel; see the module docstring for dtype routing.
+    tcgen05 kernel; see the module docstring for dtype routing.  CPU torch
+    tensors take the pipelined host path (:func:`_conv_host`; ``out`` = a
+    pinned CPU result tensor makes the call asynchronous).
     """
     cdt, odt, np_res = _plan_dtypes(x, w, compute, out_dtype)
     ordc = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[order]
+    if isinstance(x, torch.Tensor) and isinstance(w, torch.Tensor) and not x.is_cuda and not w.is_cuda:
+        if x.dim() != 4 or w.dim() != 4 or x.shape[3] != w.shape[2]:
+            raise ValueError(f"x (N,H,W,C) and w (R,S,C,K) expected, got {tuple(x.shape)} x {tuple(w.shape)}")
+        return _conv_host(x, w, (sh, sw, ph, pw, dh, dw), cdt, odt, out, tile_n=tile_n, num_ctas=num_ctas,
+                          order=ordc, flags=flags)
+    if out is not None:
+        raise ValueError("out= is for CPU (host) tensors; device calls return a new tensor")
     xd = D.to_device(x)
     wd = D.to_device(w)
     if cdt == torch.int8:

@@ -139,6 +139,32 @@ def test_halo_tiles_exact(rng, shape):
         assert np.array_equal(yi.cpu().numpy(), O.conv2d_nhwc_exact_f64(xi, wi, *args)), shape
 
 
+def test_host_tensor_path_pipelined(rng):
+    """CPU torch tensors in -> pipelined upload / conv / download (chunked over N):
+    identical to the device path, exact for integers, and ordered on the caller's stream."""
+    P = _P()
+    from oracle import oracle as O
+    x = rng.integers(-4, 5, size=(7, 40, 36, 64)).astype(np.int64)  # 7 images -> uneven chunks
+    w = rng.integers(-4, 5, size=(3, 3, 64, 96)).astype(np.int64)
+    args = (1, 1, 1, 1, 1, 1)
+    want = O.conv2d_nhwc_i64(x, w, *args)
+    hx = torch.from_numpy(x).float().bfloat16().pin_memory()
+    hw = torch.from_numpy(w).float().bfloat16().pin_memory()
+    y_dev = P._kernels.conv2d_nhwc(hx.cuda(), hw.cuda(), *args, out_dtype=torch.float32)
+    y_host = P._kernels.conv2d_nhwc(hx, hw, *args, out_dtype=torch.float32)  # allocates + syncs
+    assert not y_host.is_cuda and torch.equal(y_host, y_dev.cpu())
+    assert np.array_equal(y_host.numpy(), want.astype(np.float32))
+    out = torch.empty(y_host.shape, dtype=torch.bfloat16, pin_memory=True)
+    r = P._kernels.conv2d_nhwc(hx, hw, *args, out=out)  # asynchronous into `out`
+    assert r is out
+    torch.cuda.current_stream().synchronize()
+    assert torch.equal(out, y_dev.bfloat16().cpu())
+    yi = P._kernels.conv2d_nhwc(torch.from_numpy(x), torch.from_numpy(w), *args)  # int64 host -> int8 path
+    assert yi.dtype == torch.int32 and np.array_equal(yi.numpy(), want)
+    with pytest.raises(ValueError):
+        P._kernels.conv2d_nhwc(hx, hw, *args, out=torch.empty(3))
+
+
 @pytest.mark.parametrize("order", ["reuse_aware", "filter_major"])
 def test_subtile_orders_identical(rng, order):
     P = _P()
