@@ -41,7 +41,7 @@ constexpr int kBM = 128;           // output pixels per block (MMA M)
 constexpr int kRowBytes = 128;     // bytes of reduction per stage per row (one 128B swizzle span)
 constexpr int kAStage = kBM * kRowBytes;  // 16 KiB of A per stage
 constexpr int kThreads = 256;
-constexpr int kThreadsRowband = 288;  // conv_rowband_kernel: 4 plane-producer warps (0, 2, 3, 8), issuer, 4 epilogue warps
+constexpr int kThreadsRowband = 320;  // conv_rowband_kernel: plane producers 0/2/3/8, issuer 1, epilogue 4-7, stores 9
 constexpr int kThreadsGeneric = 320;  // + warp 8: second filter producer, warp 9: output store issuer
 
 enum ElemKind : int { ELEM_BF16 = 0, ELEM_F16 = 1, ELEM_I8 = 2 };
@@ -159,39 +159,6 @@ struct OutTraits {
     static constexpr int kBytes = (OUT == OUT_BF16 || OUT == OUT_F16) ? 2 : 4;
     static constexpr int kRowBytes = 32 * kBytes;  // one 32-column epilogue chunk of one output row
 };
-
-// Convert one row's 32 accumulator words and write them into the warp's
-// staging tile (32 rows x kRowBytes) in the TMA swizzle layout: SW64 for
-// 16-bit outputs (Swizzle<2,4,3>), SW128 for 32-bit outputs (Swizzle<3,4,3>).
-template <int OUT>
-__device__ __forceinline__ void stage_row_chunk(uint8_t *buf, uint32_t row, const uint32_t (&v)[32]) {
-    constexpr int RB = OutTraits<OUT>::kRowBytes;
-    uint8_t *dst = buf + row * RB;
-    if constexpr (OUT == OUT_BF16 || OUT == OUT_F16) {
-        uint32_t packed[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
-            if constexpr (OUT == OUT_BF16) {
-                __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
-                packed[i] = *reinterpret_cast<uint32_t *>(&t);
-            } else {
-                __half2 t = __floats2half2_rn(a, b);
-                packed[i] = *reinterpret_cast<uint32_t *>(&t);
-            }
-        }
-        const uint32_t swz = (row >> 1) & 3;
-#pragma unroll
-        for (uint32_t c = 0; c < 4; ++c)
-            *reinterpret_cast<uint4 *>(dst + ((c ^ swz) << 4)) =
-                make_uint4(packed[4 * c], packed[4 * c + 1], packed[4 * c + 2], packed[4 * c + 3]);
-    } else {
-        const uint32_t swz = row & 7;
-#pragma unroll
-        for (uint32_t c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4 *>(dst + ((c ^ swz) << 4)) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-    }
-}
 
 // One 128-byte row of a 128-row output staging tile in the SW128 TMA layout
 // (16-byte chunk c of row r lives at ((c ^ (r & 7)) * 16)): 64 bf16/fp16 or

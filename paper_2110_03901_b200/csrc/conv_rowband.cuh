@@ -86,7 +86,8 @@ template <int ELEM, int OUT, int BN, int TP>
 struct RowbandCfg {
     static constexpr int kTmemCols = 2 * TP * BN;
     static constexpr int kNChunks = BN / 64;
-    static constexpr int kStageOut = 2 * 32 * OutTraits<OUT>::kRowBytes;
+    static constexpr int kOutCols = (OUT == OUT_BF16 || OUT == OUT_F16) ? 64 : 32;  // one 128-byte chunk
+    static constexpr int kOutTile = kBM * 128;                                       // staging tile (x2)
     static_assert(ELEM != ELEM_I8, "row-band path is for 16-bit pixels of 8 channels");
     static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
 };
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *smem_b = smem;                                   // resident filter
     uint8_t *smem_out = smem + p.b_bytes;                     // epilogue staging (b_bytes is 1024-aligned)
-    uint8_t *smem_a = smem_out + 4 * Cfg::kStageOut;          // plane ring
+    uint8_t *smem_a = smem_out + 2 * Cfg::kOutTile;           // plane ring
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_a + p.n_stages * p.a_stage_bytes);
     uint64_t *full = bars;
     uint64_t *empty = bars + p.n_stages;
@@ -374,46 +375,42 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
             p.dbg[148 * 8 + blockIdx.x * 4 + 0] = t_commit;
             p.dbg[148 * 8 + blockIdx.x * 4 + 1] = t_loop;
         }
-    } else if (warp >= 4) {
-        // ---- epilogue: TP accumulators -> NHWC via 4-D TMA stores ----
+    } else if (warp >= 4 && warp < 8) {
+        // ---- epilogue: per output row j and 128-byte channel chunk, the four warps stage
+        // the block's 128 pixels as one SW128 tile and the store warp writes it with ONE
+        // 4-D TMA store {chunk, 128 pixels (clipped at Q), 1 row, 1 image}; handshake as in
+        // conv_fwd_kernel (named barriers FULL(b) = 1 + b, EMPTY(b) = 3 + b) ----
         const int quarter = warp & 3;
-        uint8_t *stage_buf = smem_out + quarter * Cfg::kStageOut;
-        constexpr int kBuf = 32 * OutTraits<OUT>::kRowBytes;
+        const uint32_t row = quarter * 32 + lane;
+        constexpr int kOC = Cfg::kOutCols;
         int acc = 0;
         uint32_t acc_phase = 0;
         uint32_t chunk_ctr = 0;
         long long w_tfull = 0;
         const long long t_start = clock64();
         for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-            const int qb = static_cast<int>(tile % p.q_blocks);
             const long long rest = tile / p.q_blocks;
             const int pg = static_cast<int>(rest % p.p_groups);
-            const int n = static_cast<int>(rest / p.p_groups);
-            const int qrow = qb * 128 + quarter * 32;
             timed_wait(&tfull[acc], acc_phase, w_tfull, (p.dbg_flags & 64) ? 200 : 0);
             ptx::tc_fence_after();
 #pragma unroll 1
             for (int j = 0; j < TP; ++j) {
-                const int prow = pg * TP + j;
+                if (pg * TP + j >= p.p) continue;  // uniform (the store warp skips it too)
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
-                    uint32_t v[32];
-                    if (IMCONV_INSTRUMENT && (p.dbg_flags & 1)) continue;
+                for (int c = 0; c < BN / kOC; ++c) {
+                    if (c * kOC >= p.k) continue;
+                    uint32_t v[kOC];
                     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                           static_cast<uint32_t>(acc * TP * BN + j * BN + c * 32);
-                    ptx::tmem_ld_32x32b_x32(taddr, v);
+                                           static_cast<uint32_t>(acc * TP * BN + j * BN + c * kOC);
+#pragma unroll
+                    for (int h = 0; h < kOC / 32; ++h)
+                        ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
                     ptx::tmem_ld_wait();
-                    if (prow >= p.p || qrow >= p.q || c * 32 >= p.k) continue;  // warp-uniform
-                    uint8_t *buf = stage_buf + (chunk_ctr & 1) * kBuf;
-                    if (lane == 0) ptx::tma_store_wait_read<1>();
-                    __syncwarp();
-                    stage_row_chunk<OUT>(buf, lane, v);
+                    const uint32_t b = chunk_ctr & 1;
+                    if (chunk_ctr >= 2) ptx::named_bar_sync(3 + b, 160);  // EMPTY(b)
+                    if (!(IMCONV_INSTRUMENT && (p.dbg_flags & 1))) stage_row128<OUT>(smem_out + b * Cfg::kOutTile, row, v);
                     ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        ptx::tma_store_4d(&tmap_y, buf, c * 32, qrow, prow, n);
-                        ptx::tma_store_commit();
-                    }
+                    ptx::named_bar_arrive(1 + b, 160);  // FULL(b)
                     ++chunk_ctr;
                 }
             }
@@ -423,12 +420,40 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if (lane == 0) ptx::tma_store_wait<0>();
-        __syncwarp();
+        if (chunk_ctr >= 2) ptx::named_bar_sync(3 + (chunk_ctr & 1), 160);
         if (IMCONV_INSTRUMENT && p.dbg && lane == 0 && quarter == 0) {
             p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 6] = w_tfull;
         }
+    } else if (warp == 9) {
+        // ---- output store issuer ----
+        constexpr int kOC = Cfg::kOutCols;
+        uint32_t chunk_ctr = 0;
+        for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            const int qb = static_cast<int>(tile % p.q_blocks);
+            const long long rest = tile / p.q_blocks;
+            const int pg = static_cast<int>(rest % p.p_groups);
+            const int n = static_cast<int>(rest / p.p_groups);
+            for (int j = 0; j < TP; ++j) {
+                const int prow = pg * TP + j;
+                if (prow >= p.p) continue;
+                for (int c = 0; c < BN / kOC; ++c) {
+                    if (c * kOC >= p.k) continue;
+                    const uint32_t b = chunk_ctr & 1;
+                    ptx::named_bar_sync(1 + b, 160);  // FULL(b)
+                    if (lane == 0) {
+                        ptx::tma_store_4d(&tmap_y, smem_out + b * Cfg::kOutTile, c * kOC, qb * 128, prow, n);
+                        ptx::tma_store_commit();
+                        ptx::tma_store_wait_read<1>();
+                    }
+                    __syncwarp();
+                    if (chunk_ctr >= 1) ptx::named_bar_arrive(3 + (b ^ 1), 160);  // EMPTY(b ^ 1)
+                    ++chunk_ctr;
+                }
+            }
+        }
+        if (lane == 0) ptx::tma_store_wait<0>();
+        __syncwarp();
     }
 
     __syncthreads();

@@ -397,8 +397,8 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     p.npairs = (S + 1) / 2;
     p.b_chunk_bytes = R * p.npairs * 2 * 1024;
     p.b_bytes = (BN / 64) * p.b_chunk_bytes;
-    const int kStageOut = 2 * 32 * ((a->out_dtype == IMCONV_F32) ? 128 : 64);
-    const int fixed = p.b_bytes + 4 * kStageOut + 1024 /*align*/ + 1024 /*barriers + tables*/;
+    const int kStaging = 2 * kBM * 128;  // two 128-pixel x 128-byte epilogue staging tiles
+    const int fixed = p.b_bytes + kStaging + 1024 /*align*/ + 1024 /*barriers + tables*/;
     const int room = kMaxDynSmem - fixed;
     // input rows per pipeline stage: every stage costs the MMA issuer a fixed
     // handshake (wait, fences, commit), so stages are made as large as the
@@ -459,10 +459,10 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
                               static_cast<cuuint64_t>(N)};
         cuuint64_t gstride[3] = {static_cast<cuuint64_t>(K * eo), static_cast<cuuint64_t>(Q * K * eo),
                                  static_cast<cuuint64_t>(P * Q * K * eo)};
-        cuuint32_t box[4] = {32, 32, 1, 1};
+        cuuint32_t box[4] = {static_cast<cuuint32_t>(128 / eo), 128, 1, 1};  // one 128-byte chunk x 128 pixels
         cuuint32_t es[4] = {1, 1, 1, 1};
         if (g_encode_tiled(&ty, dt, 4, a->y, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           eo == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return IMCONV_ETMAP;
     }
