@@ -68,6 +68,11 @@ struct ConvParams {
     int b_3d;            // 1: the filter map is 3-D {chunk cols, rows, chunks}: one TMA per stage for all of B
     int a_gather;        // 1: 16-byte pixels -- A tap blocks gathered by cp.async warps instead of TMA
     const uint8_t *x;    // NHWC input (gather mode)
+    int sk_split;        // split-K tail: S > 1 splits each of the last (total - sk_first) tiles' k-loop S ways
+    long long sk_first;  // first tail tile (a multiple of the grid: the full waves end here)
+    float *sk_ws;        // fp32 partials [tail tile][S][MT*128 rows][BN]
+    unsigned long long *sk_cnt;  // per tail tile arrival counters, tagged (sk_gen << 8) | count
+    unsigned long long sk_gen;   // launch generation (counters never need clearing)
     int b_resident;      // 1: grid is a multiple of n_tiles (each CTA keeps one output-channel block) --
                          //    when a block's k-subtiles fit the B ring, its filter slice is loaded once
     int a_tiled;         // 1: 1x1 / stride 1 / no padding -- A is the plain (M x C) matrix, loaded with
@@ -107,6 +112,46 @@ struct KWalk {
         }
     }
 };
+
+// Work units of one persistent CTA (round-robin over the grid): whole tiles
+// [0, full_end), then -- split-K tail -- unit v = u - full_end < tail*S is
+// split v % S of tile full_end + v / S over k-stages [kb0, kb1).  Every role
+// walks the same sequence.
+struct Unit {
+    long long tile;
+    int kb0, kb1, split;  // split < 0: the whole tile
+};
+__device__ __forceinline__ bool get_unit(long long u, long long full_end, long long total, int S, int k_stages,
+                                         Unit &w) {
+    if (u < full_end) {
+        w.tile = u;
+        w.kb0 = 0;
+        w.kb1 = k_stages;
+        w.split = -1;
+        return true;
+    }
+    if (S <= 1) return false;
+    const long long v = u - full_end;
+    if (v >= (total - full_end) * S) return false;
+    w.tile = full_end + v / S;
+    w.split = static_cast<int>(v % S);
+    w.kb0 = w.split * k_stages / S;
+    w.kb1 = (w.split + 1) * k_stages / S;
+    return true;
+}
+
+// Arrival of one split on its tail tile's counter; true for the last (S-th)
+// arrival of this launch.  Counters are tagged with the launch generation, so
+// a stale value from an earlier launch restarts the count at 1.
+__device__ __forceinline__ bool sk_arrive(unsigned long long *slot, unsigned long long gen, int S) {
+    unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(slot);
+    while (true) {
+        const unsigned long long nv = (cur >> 8) == gen ? cur + 1 : ((gen << 8) | 1ull);
+        const unsigned long long prev = atomicCAS(slot, cur, nv);
+        if (prev == cur) return static_cast<int>(nv & 0xff) == S;
+        cur = prev;
+    }
+}
 
 // Instrumentation (IMCONV_INSTRUMENT builds only, libimconv_instr.so): cycles
 // spent in blocking waits per role; production builds compile to a plain wait.
@@ -250,6 +295,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     uint64_t *tempty = tfull + 2;
     uint64_t *bres = tempty + 2;  // resident filter slice landed (B-stationary mode)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres + 1);
+    volatile uint32_t *sk_last = tmem_slot + 2;  // split-K: this CTA's split was the last of its tile
 
     // broadcast from lane 0: the role branches are then provably warp-uniform and
     // ptxas keeps the MMA issuer's descriptors on the uniform datapath
@@ -267,6 +313,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     // and all k-subtiles of a block fit the B ring -> the filter slice is loaded
     // once into ring slots 0..k_stages-1 and only A streams (1x1 layers, C*e <= 4*128 B)
     const bool b_res = CG == 1 && KSUB == 1 && p.b_resident && !p.a_gather && k_stages <= STAGES;
+    // split-K tail (host guarantees sk_first is a multiple of the grid)
+    const int S = (CG == 1 && !p.a_gather && !b_res && p.sk_split > 1) ? p.sk_split : 1;
+    const long long full_end = S > 1 ? p.sk_first : total_tiles;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmap_a);
@@ -417,7 +466,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             long long w_empty = 0;
             const long long t_start = clock64();
             KWalk kw;
-            for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
+            Unit wu;
+            for (long long ui = tile_start; get_unit(ui, full_end, total_tiles, S, k_stages, wu); ui += tile_step) {
+                const long long tile = wu.tile;
                 const long long m_tile = tile / p.n_tiles;
                 const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
                 const long long m0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows;
@@ -429,7 +480,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                 const int h0 = p0 * p.sh - p.ph;
                 const int nb0 = n_tile * BN + static_cast<int>(rank) * (BN / CG);
                 kw.reset();
-                for (int kb = 0; kb < k_stages; ++kb) {
+                for (int i = 0; i < wu.kb0 * KSUB && p.tps == 1; ++i) kw.next(p.order, p.r, p.s, p.c_chunks);
+                for (int kb = wu.kb0; kb < wu.kb1; ++kb) {
                     const bool mine = ((it++) & 1u) == static_cast<uint32_t>(par);
                     const int nsub = min(KSUB, k_subs - kb * KSUB);
                     // completion barrier: own `full` (single CTA) or the leader's (pair)
@@ -569,11 +621,12 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         long long w_tempty = 0, w_full = 0;
         if (b_res) ptx::mbar_wait(bres, 0);
         const long long t_start = clock64();
-        for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
+        Unit wu;
+        for (long long ui = tile_start; get_unit(ui, full_end, total_tiles, S, k_stages, wu); ui += tile_step) {
             timed_wait_g(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
             const uint32_t d_base = tmem_u + static_cast<uint32_t>(acc * MT * BN);
-            for (int kb = 0; kb < k_stages; ++kb) {
+            for (int kb = wu.kb0; kb < wu.kb1; ++kb) {
                 timed_wait_g(&full[stage], phase, w_full);
                 ptx::tc_fence_after();
                 {
@@ -587,7 +640,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                             for (int kk = 0; kk < Cfg::kMmaPerSub; ++kk) {
                                 const uint64_t bdesc =
                                     b_st + static_cast<uint64_t>((u * Cfg::kBSub + kk * Cfg::kMmaK * kRowBytes) >> 4);
-                                const uint32_t accum = (kb | u | kk) != 0 ? 1u : 0u;
+                                const uint32_t accum = (kb != wu.kb0 || (u | kk) != 0) ? 1u : 0u;
 #pragma unroll
                                 for (int mt = 0; mt < MT; ++mt) {
                                     const uint64_t adesc =
@@ -647,49 +700,116 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         uint32_t chunk_ctr = 0;
         long long w_tfull = 0, t_ld = 0, t_bar = 0, t_st = 0;
         const long long t_start = clock64();
-        for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
+        // hand one staged 128 x 128-byte chunk (fp32 / int32 words v) to the store warp
+        auto stage_chunk = [&](const uint32_t *v) {
+            const uint32_t b = chunk_ctr & 1;
+            if (chunk_ctr >= 2) ptx::named_bar_sync(3 + b, 160);  // EMPTY(b)
+            stage_row128<OUT>(smem_out + b * Cfg::kOutTile, row, v);
+            ptx::fence_proxy_async_smem();
+            ptx::named_bar_arrive(1 + b, 160);  // FULL(b)
+            ++chunk_ctr;
+        };
+        Unit wu;
+        for (long long ui = tile_start; get_unit(ui, full_end, total_tiles, S, k_stages, wu); ui += tile_step) {
+            const long long tile = wu.tile;
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
             timed_wait_g(&tfull[acc], acc_phase, w_tfull);
             ptx::tc_fence_after();
+            if (wu.split < 0) {
 #pragma unroll 1
-            for (int mt = 0; mt < MT; ++mt) {
-                const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;
+                for (int mt = 0; mt < MT; ++mt) {
+                    const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;
 #pragma unroll 1
-                for (int j = 0; j < BN / kOC; ++j) {
-                    const int col0 = n_tile * BN + j * kOC;
-                    if (col0 >= p.k || row0 >= p.m) continue;  // uniform (the store warp skips it too)
-                    uint32_t v[kOC];
-                    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                           static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC);
-                    const long long e0 = IMCONV_INSTRUMENT ? clock64() : 0;
+                    for (int j = 0; j < BN / kOC; ++j) {
+                        const int col0 = n_tile * BN + j * kOC;
+                        if (col0 >= p.k || row0 >= p.m) continue;  // uniform (the store warp skips it too)
+                        uint32_t v[kOC];
+                        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                               static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC);
+                        const long long e0 = IMCONV_INSTRUMENT ? clock64() : 0;
 #pragma unroll
-                    for (int h = 0; h < kOC / 32; ++h)
-                        ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
-                    ptx::tmem_ld_wait();
-                    const long long e1 = IMCONV_INSTRUMENT ? clock64() : 0;
-                    const uint32_t b = chunk_ctr & 1;
-                    if (chunk_ctr >= 2) ptx::named_bar_sync(3 + b, 160);  // EMPTY(b)
-                    const long long e2 = IMCONV_INSTRUMENT ? clock64() : 0;
-                    stage_row128<OUT>(smem_out + b * Cfg::kOutTile, row, v);
-                    ptx::fence_proxy_async_smem();
-                    ptx::named_bar_arrive(1 + b, 160);  // FULL(b)
-                    if (IMCONV_INSTRUMENT) {
-                        t_ld += e1 - e0;
-                        t_bar += e2 - e1;
-                        t_st += clock64() - e2;
+                        for (int h = 0; h < kOC / 32; ++h)
+                            ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
+                        ptx::tmem_ld_wait();
+                        const long long e1 = IMCONV_INSTRUMENT ? clock64() : 0;
+                        stage_chunk(v);
+                        if (IMCONV_INSTRUMENT) {
+                            t_ld += e1 - e0;
+                            t_st += clock64() - e1;
+                        }
                     }
-                    ++chunk_ctr;
                 }
-            }
-            // every TMEM load of this accumulator has completed: release it
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if constexpr (CG == 2)
-                    ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
-                else
-                    ptx::mbar_arrive(&tempty[acc]);
+                // every TMEM load of this accumulator has completed: release it
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2)
+                        ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+                    else
+                        ptx::mbar_arrive(&tempty[acc]);
+                }
+            } else {
+                // ---- split-K tail unit: raw 32-bit partial sums -> workspace [tile][split][row][BN];
+                // the split that arrives last on the tile's counter adds all S partials and stores ----
+                const long long tt = tile - full_end;
+                uint32_t *ws_tile = reinterpret_cast<uint32_t *>(p.sk_ws) + tt * S * (Cfg::kRows * BN);
+                uint32_t *ws_mine = ws_tile + static_cast<long long>(wu.split) * (Cfg::kRows * BN);
+#pragma unroll 1
+                for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll 1
+                    for (int j = 0; j < BN / 32; ++j) {
+                        uint32_t v[32];
+                        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                                    static_cast<uint32_t>(acc * MT * BN + mt * BN + j * 32),
+                                                v);
+                        ptx::tmem_ld_wait();
+                        uint4 *dst = reinterpret_cast<uint4 *>(ws_mine + static_cast<long long>(mt * kBM + row) * BN +
+                                                               j * 32);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                __threadfence();                      // this thread's partial is visible GPU-wide ...
+                ptx::named_bar_sync(5, 128);          // ... for all four epilogue warps
+                if (warp == 4 && lane == 0) *sk_last = sk_arrive(p.sk_cnt + tt, p.sk_gen, S) ? 1u : 0u;
+                ptx::named_bar_sync(6, 160);          // decision -> epilogue warps and the store warp
+                if (*sk_last) {
+                    __threadfence();
+#pragma unroll 1
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const long long row0 = m_tile * Cfg::kRows + mt * kBM;
+#pragma unroll 1
+                        for (int j = 0; j < BN / kOC; ++j) {
+                            const int col0 = n_tile * BN + j * kOC;
+                            if (col0 >= p.k || row0 >= p.m) continue;
+                            uint32_t v[kOC];
+#pragma unroll
+                            for (int q = 0; q < kOC; ++q) v[q] = 0u;
+                            for (int s2 = 0; s2 < S; ++s2) {
+                                const uint4 *src = reinterpret_cast<const uint4 *>(
+                                    ws_tile + (static_cast<long long>(s2) * Cfg::kRows + mt * kBM + row) * BN + j * kOC);
+#pragma unroll
+                                for (int q = 0; q < kOC / 4; ++q) {
+                                    const uint4 t4 = __ldcg(src + q);
+                                    const uint32_t t[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        if constexpr (OUT == OUT_I32)
+                                            v[4 * q + e] += t[e];  // int32 two's complement
+                                        else
+                                            v[4 * q + e] = __float_as_uint(__uint_as_float(v[4 * q + e]) +
+                                                                           __uint_as_float(t[e]));
+                                    }
+                                }
+                            }
+                            stage_chunk(v);
+                        }
+                    }
+                }
             }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
@@ -708,9 +828,15 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         // ===== output store issuer: one TMA store per staged 128 x 128-byte tile =====
         constexpr int kOC = Cfg::kOutCols;
         uint32_t chunk_ctr = 0;
-        for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
+        Unit wu;
+        for (long long ui = tile_start; get_unit(ui, full_end, total_tiles, S, k_stages, wu); ui += tile_step) {
+            const long long tile = wu.tile;
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
+            if (wu.split >= 0) {  // split-K unit: only the last split of the tile stores it
+                ptx::named_bar_sync(6, 160);
+                if (!*sk_last) continue;
+            }
             for (int mt = 0; mt < MT; ++mt) {
                 const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;
                 for (int j = 0; j < BN / kOC; ++j) {

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <type_traits>
 
@@ -32,6 +33,28 @@ int g_debug_flags = 0;
 constexpr int kDbgNoTiledA = 1 << 16;     // 1x1 stride-1 layers keep the im2col A map
 constexpr int kDbgNoBResident = 1 << 17;  // never load the filter slice once per CTA
 constexpr int kDbgNoPdl = 1 << 18;        // launch without programmatic stream serialization
+constexpr int kDbgNoSplitK = 1 << 19;     // never split the tail wave's k-loops
+
+// Split-K arrival counters: one per tail tile, tagged with a launch generation
+// so they never need clearing; each launch uses one of 256 slices (so up to
+// 256 launches may be in flight on different streams without sharing one).
+std::mutex g_sk_mutex;
+unsigned long long *g_sk_counters[64] = {};
+std::atomic<unsigned long long> g_sk_gen{1};
+constexpr int kSkSlices = 256, kSkSliceLen = 256;
+
+unsigned long long *sk_counters(int dev) {
+    std::lock_guard<std::mutex> lock(g_sk_mutex);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!g_sk_counters[dev]) {
+        void *ptr = nullptr;
+        const size_t bytes = sizeof(unsigned long long) * kSkSlices * kSkSliceLen;
+        if (cudaMalloc(&ptr, bytes) != cudaSuccess) return nullptr;
+        if (cudaMemset(ptr, 0, bytes) != cudaSuccess) return nullptr;
+        g_sk_counters[dev] = static_cast<unsigned long long *>(ptr);
+    }
+    return g_sk_counters[dev];
+}
 
 std::mutex g_mu;
 PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
@@ -777,19 +800,60 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         }
     }
 
-    if (grid > tiles) grid = static_cast<int>(tiles);
+    // Split-K tail: when the last wave would be at most half full, each of its
+    // `tail` tiles is split into S k-ranges run by S CTAs (S*tail <= grid); the
+    // partial sums meet in an fp32/int32 workspace and the last split stores.
+    // The full waves stay data-parallel.  (Not with B-stationary: split units
+    // change a CTA's output-channel block.)
+    void *sk_ws = nullptr;
+    p.sk_split = 1;
+    if (!use_pair && !p.a_gather && !p.b_resident && !(g_debug_flags & kDbgNoSplitK)) {
+        const int ksub = variant == 1 ? 2 : 1;
+        const int k_st = (p.k_stages + ksub - 1) / ksub;
+        const long long g0 = grid;
+        const long long tail = tiles >= g0 ? tiles % g0 : tiles;
+        // measured: pays only when the tail wave is a large share of the work (at most
+        // two waves) and each tile's k-loop is long enough to amortise the partial
+        // write + reduce (s5 3x3: 55.5 -> 48.3 us; 5-wave s3 layers lose)
+        constexpr int kSkMinStages = 36;
+        if (tail > 0 && 2 * tail <= g0 && tiles < 2 * g0 && k_st >= kSkMinStages) {
+            const int S = static_cast<int>(std::min<long long>({g0 / tail, static_cast<long long>(k_st), 4}));
+            int dev = 0;
+            cudaGetDevice(&dev);
+            unsigned long long *cnt = S >= 2 ? sk_counters(dev) : nullptr;
+            const size_t ws_bytes = static_cast<size_t>(tail) * S * (kBM * mt) * bn * 4;
+            if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
+                const unsigned long long gen = g_sk_gen.fetch_add(1);
+                p.sk_split = S;
+                p.sk_first = tiles - tail;
+                p.sk_ws = static_cast<float *>(sk_ws);
+                p.sk_gen = gen;
+                p.sk_cnt = cnt + (gen % kSkSlices) * kSkSliceLen;
+                if (tiles < g0) grid = static_cast<int>(tail * S);
+            } else {
+                sk_ws = nullptr;
+                cudaGetLastError();  // (allocation failure: run without splitting)
+            }
+        }
+    }
+    if (p.sk_split == 1 && grid > tiles) grid = static_cast<int>(tiles);
+    int rc_launch;
     switch (a->in_dtype) {
         case IMCONV_BF16:
-            return a->out_dtype == IMCONV_F32
+            rc_launch = a->out_dtype == IMCONV_F32
                        ? dispatch_bn<ELEM_BF16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
                        : dispatch_bn<ELEM_BF16, OUT_BF16>(bn, variant, ta, tb, ty, p, grid, st);
+            break;
         case IMCONV_F16:
-            return a->out_dtype == IMCONV_F32
-                       ? dispatch_bn<ELEM_F16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
-                       : dispatch_bn<ELEM_F16, OUT_F16>(bn, variant, ta, tb, ty, p, grid, st);
-        case IMCONV_I8: return dispatch_bn<ELEM_I8, OUT_I32>(bn, variant, ta, tb, ty, p, grid, st);
-        default: return IMCONV_EDTYPE;
+            rc_launch = a->out_dtype == IMCONV_F32
+                            ? dispatch_bn<ELEM_F16, OUT_F32>(bn, variant, ta, tb, ty, p, grid, st)
+                            : dispatch_bn<ELEM_F16, OUT_F16>(bn, variant, ta, tb, ty, p, grid, st);
+            break;
+        case IMCONV_I8: rc_launch = dispatch_bn<ELEM_I8, OUT_I32>(bn, variant, ta, tb, ty, p, grid, st); break;
+        default: rc_launch = IMCONV_EDTYPE;
     }
+    if (sk_ws) cudaFreeAsync(sk_ws, st);  // stream-ordered: released after the kernel
+    return rc_launch;
 }
 
 int imconv_gemm(const void *A, const void *B, void *Cm, int32_t in_dtype, int32_t out_dtype, int64_t m, int64_t kd,

@@ -139,6 +139,35 @@ def test_halo_tiles_exact(rng, shape):
         assert np.array_equal(yi.cpu().numpy(), O.conv2d_nhwc_exact_f64(xi, wi, *args)), shape
 
 
+@pytest.mark.parametrize("shape", [(1, 7, 7, 512, 512), (3, 9, 5, 512, 320), (2, 14, 14, 512, 256)])
+def test_split_k_tail_exact(rng, shape):
+    """Long k-loops with a short last wave run split-K (S k-ranges per tail tile, partials
+    summed by the last arriving split): exact, repeatable across launches (generation-tagged
+    counters), and equal to the unsplit kernel."""
+    P = _P()
+    from oracle import oracle as O
+    n, h, w_, c, k = shape
+    args = (1, 1, 1, 1, 1, 1)
+    x = rng.integers(-2, 3, size=(n, h, w_, c)).astype(np.int64)
+    w = rng.integers(-2, 3, size=(3, 3, c, k)).astype(np.int64)
+    want = O.conv2d_nhwc_exact_f64(x, w, *args).astype(np.int64)
+    xb = torch.from_numpy(x).float().cuda().bfloat16()
+    wb = torch.from_numpy(w).float().cuda().bfloat16()
+    ys = [P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32) for _ in range(3)]
+    for y in ys:
+        assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), shape
+    P._lib.lib.imconv_debug_set_flags(1 << 19)  # split-K off
+    try:
+        y_ref = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    finally:
+        P._lib.lib.imconv_debug_set_flags(0)
+    assert torch.equal(ys[0], y_ref)
+    xi = torch.from_numpy(x).to(torch.int8).cuda()
+    wi = torch.from_numpy(w).to(torch.int8).cuda()
+    yi = P._kernels.conv2d_nhwc(xi, wi, *args)
+    assert np.array_equal(yi.cpu().numpy(), want), shape
+
+
 def test_host_tensor_path_pipelined(rng):
     """CPU torch tensors in -> pipelined upload / conv / download (chunked over N):
     identical to the device path, exact for integers, and ordered on the caller's stream."""

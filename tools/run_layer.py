@@ -55,7 +55,7 @@ def run_one(args, layer):
         x = torch.randn((sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev).to(torch.bfloat16)
         w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev) * 0.05).to(torch.bfloat16)
     order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[args.order]
-    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8))
+    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8) | int(os.environ.get("IMCONV_DEBUG_FLAGS", "0"), 0))
     def once():
         if args.explicit:
             low = K.im2col_nhwc(x, sp.h_f, sp.w_f, *sp.conv_args(), True)
