@@ -615,7 +615,10 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     // (A wave-quantisation chooser over {256x128, 128x256, 128x128, ...} blocks
     // was measured worse on the stage-5 layers: smaller blocks lose more
     // per-block efficiency than they gain in wave fill, so BN is fixed by K.)
-    const int auto_variant = -1;
+    // 1x1 layers with N = 128: one m-tile per CTA and two k-subtiles per stage measured
+    // faster than two m-tiles (s3 1x1a: 102.5 -> 94.0 us, 44.8 -> 43.7 us); 3x3 and N = 64 lose.
+    const bool no_override = !(a->flags & (IMCONV_FLAG_KSUB1 | IMCONV_FLAG_MT1));
+    const int auto_variant = (no_override && R * S == 1 && bn == 128) ? 1 : -1;
 
     // ---- block shape: single CTA or CTA pair (cta_group::2, B split across the pair) ----
     // pairs need whole swizzle-atom columns per CTA (BN >= 128 bf16 / 256 int8)
