@@ -220,15 +220,59 @@ __global__ void __launch_bounds__(256, 1) pipe_replay(int stages, int mps, int l
         }
         for (int u = 0; u < np; ++u) ptx::mbar_arrive(&full[pend[u]]);
     } else if (warp == 0 && (!(variant & 8) || lane == 0)) {
+        // (variant 256: the a0 region holds 4 SW128 A tiles of 16 KB for the uniform issuer)
         long long t0 = clock64();
         long long tw = 0;
+        bool ready = false;  // variant 512: stage st's full barrier already seen complete (look-ahead)
         for (int st = 0; st < stages; ++st) {
             const int s = st % nst;
             const long long ta = clock64();
-            if (!(variant & 64) && (!(variant & 2) || lane == 0)) ptx::mbar_wait(&full[s], (st / nst) & 1);
+            if (!(variant & 64) && (!(variant & 2) || lane == 0) && !ready) ptx::mbar_wait(&full[s], (st / nst) & 1);
             tw += clock64() - ta;
+            if (variant & 512) {
+                const uint32_t a_u = __shfl_sync(0xffffffffu, a0, 0), b_u = __shfl_sync(0xffffffffu, b0, 0);
+                const uint32_t t_u = __shfl_sync(0xffffffffu, tbase, 0);
+                const uint64_t ad0 = ptx::smem_desc(a_u + (s % 4) * 16384, 16, 1024, ptx::LAYOUT_SW128);
+                const uint64_t bd0 = ptx::smem_desc(b_u, 8192, 1024, ptx::LAYOUT_SW128);
+                ptx::tc_fence_after();
+                for (int k = 0; k < mps; ++k) {
+                    ptx::mma_f16_elect(t_u, ad0 + static_cast<uint64_t>((k & 3) * 2), bd0 + static_cast<uint64_t>((k & 3) * 128),
+                                       idesc, 1);
+                    if (k == mps / 2 - 1) {
+                        const int sn = (st + 1) % nst;
+                        if (variant & 4096) {  // blocking wait for the next stage, hidden behind this stage's last MMAs
+                            if (st + 1 < stages) ptx::mbar_wait(&full[sn], ((st + 1) / nst) & 1);
+                            ready = true;
+                        } else {
+                            ready = st + 1 < stages && ptx::mbar_test_wait(ptx::smem_u32(&full[sn]), ((st + 1) / nst) & 1);
+                        }
+                    }
+                }
+                ptx::mma_commit_elect(&empty[s]);
+                continue;
+            }
             if (!(variant & 1)) ptx::tc_fence_after();
-            if (variant & 128) {
+            if (variant & 256) {
+                // the production issuer: whole warp, warp-uniform descriptors (uniform datapath)
+                const uint32_t a_u = __shfl_sync(0xffffffffu, a0, 0), b_u = __shfl_sync(0xffffffffu, b0, 0);
+                const uint32_t t_u = __shfl_sync(0xffffffffu, tbase, 0);
+                const uint64_t ad0 = ptx::smem_desc(a_u + (s % 4) * 16384, 16, 1024, ptx::LAYOUT_SW128);
+                const uint64_t bd0 = ptx::smem_desc(b_u, 8192, 1024, ptx::LAYOUT_SW128);
+                for (int k = 0; k < mps; ++k)
+                    ptx::mma_f16_elect(t_u, ad0 + static_cast<uint64_t>((k & 3) * 2), bd0 + static_cast<uint64_t>((k & 3) * 128),
+                                       idesc, 1);
+                if (variant & 1024) {
+                    // one commit per pair of stages (arrives on both stages' empty barriers in turn)
+                    if (st & 1) {
+                        ptx::mma_commit_elect(&empty[(st - 1) % nst]);
+                        ptx::mma_commit_elect(&empty[s]);
+                    }
+                } else if (variant & 2048) {
+                    // no commit at all in the loop (producer never waits: lag large) -- lower bound
+                } else {
+                    ptx::mma_commit_elect(&empty[s]);
+                }
+            } else if (variant & 128) {
                 const uint32_t a_st = a0 + s * 4352;
                 for (int k = 0; k < mps; ++k) {
                     const uint64_t adesc = ptx::smem_desc(a_st + 16 + (k & 3) * 32, 16, 128, ptx::LAYOUT_NONE);
@@ -297,11 +341,15 @@ void run(const char *name) {
 }
 
 int main() {
+    // pipe replay of the production issuer (variant 256: uniform datapath), N = 256:
+    //   +64 = no full-barrier wait, +1 = no tcgen05 fence -> which part of the per-stage handshake costs
+    for (int mps : {4, 8, 16})
+        for (int v : {256, 256 + 64, 256 + 64 + 2048 + 32}) run_pipe(mps, 4, 1, v, 256);
+    return 0;
     run_replay(0);
     for (int v : {0, 128}) run_pipe(4, 4, 1, v, 256);
     for (int v : {0, 128}) run_pipe(8, 4, 1, v, 256);
     for (int v : {0, 128}) run_pipe(4, 4, 1, v, 128);
-    return 0;
     run<64, 0>("SS  A=SW128");
     run<128, 0>("SS  A=SW128");
     run<256, 0>("SS  A=SW128");
