@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define IMCONV_ABI_VERSION 1
+#define IMCONV_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define IMCONV_API __attribute__((visibility("default")))
@@ -155,6 +155,35 @@ IMCONV_API int imconv_pad_copy(const void *src, void *dst, int32_t elem_bytes, i
  */
 IMCONV_API int imconv_lru_simulate(const int64_t *keys, int64_t count, int64_t capacity,
                         int64_t *hits, int64_t *misses);
+
+/*
+ * DRAM-traffic prediction for the generic kernel's actual B200 raster (host
+ * code, no GPU needed).  Replays the schedule
+ * imconv_conv2d_nhwc would run -- the same block shape, persistent round-robin
+ * over `sms` CTAs (all CTAs advanced stage by stage in lockstep), the
+ * k-subtile order of a->order, B-stationary and split-K decisions -- as a
+ * stream of 128-byte line accesses (NHWC activations with batch-aware
+ * addresses, HWCN filter, NHWC output), through a fully-associative
+ * write-back LRU of l2_bytes.  Reads that miss are DRAM reads; dirty output
+ * lines evicted during the kernel are DRAM writes; dirty lines still resident
+ * at the end are reported separately (an ncu launch list with a flushed L2
+ * counts them only when they are evicted later).  Extends the reference's
+ * reuse_traffic model (blocksched.py:102-151, keys without the batch) to the
+ * GPU schedule.  x/w/y pointers are ignored.
+ */
+typedef struct imconv_traffic {
+    int64_t dram_read_bytes;       /* predicted DRAM reads */
+    int64_t dram_write_bytes;      /* dirty lines evicted during the kernel */
+    int64_t resident_dirty_bytes;  /* output bytes still in L2 at the end */
+    int64_t line_requests;         /* 128-byte line accesses (A + B + y) */
+    int64_t compulsory_read_bytes; /* distinct A and B lines touched x 128 */
+    int64_t tiles;                 /* output blocks */
+    int32_t bn, mt, grid, k_subtiles;
+    int32_t kernel;                /* kernel imconv_conv2d_nhwc picks: 0 generic, 1 row-band, 2 halo
+                                      (the replay always models the generic raster) */
+} imconv_traffic;
+IMCONV_API int imconv_predict_traffic(const imconv_conv_args *args, int64_t l2_bytes, int32_t sms,
+                                      imconv_traffic *out);
 
 /* Device / build introspection (no compute). */
 IMCONV_API int imconv_abi_version(void);

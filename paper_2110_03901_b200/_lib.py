@@ -25,7 +25,7 @@ EXPORTED = (
     "imconv_conv2d_nhwc", "imconv_out_extent", "imconv_gemm", "imconv_tile_gather_nhwc",
     "imconv_im2col_nhwc", "imconv_pad_copy", "imconv_lru_simulate", "imconv_abi_version",
     "imconv_device_sm_count", "imconv_strerror", "imconv_launch_count", "imconv_reset_launch_count",
-    "imconv_debug_set_buffer", "imconv_debug_set_flags",
+    "imconv_debug_set_buffer", "imconv_debug_set_flags", "imconv_predict_traffic",
 )
 
 
@@ -42,6 +42,18 @@ class ImconvArgs(ctypes.Structure):
         ("dil_h", ctypes.c_int32), ("dil_w", ctypes.c_int32),
         ("tile_n", ctypes.c_int32), ("num_ctas", ctypes.c_int32),
         ("order", ctypes.c_int32), ("flags", ctypes.c_int32),
+    ]
+
+
+class ImconvTraffic(ctypes.Structure):
+    """Mirror of imconv_traffic (include/imconv.h)."""
+
+    _fields_ = [
+        ("dram_read_bytes", ctypes.c_int64), ("dram_write_bytes", ctypes.c_int64),
+        ("resident_dirty_bytes", ctypes.c_int64), ("line_requests", ctypes.c_int64),
+        ("compulsory_read_bytes", ctypes.c_int64), ("tiles", ctypes.c_int64),
+        ("bn", ctypes.c_int32), ("mt", ctypes.c_int32), ("grid", ctypes.c_int32), ("k_subtiles", ctypes.c_int32),
+        ("kernel", ctypes.c_int32),
     ]
 
 
@@ -86,6 +98,8 @@ def _load():
     L.imconv_debug_set_buffer.restype = None
     L.imconv_debug_set_flags.argtypes = [ctypes.c_int]
     L.imconv_debug_set_flags.restype = None
+    L.imconv_predict_traffic.argtypes = [ctypes.POINTER(ImconvArgs), i64, i32, ctypes.POINTER(ImconvTraffic)]
+    L.imconv_predict_traffic.restype = ctypes.c_int
     return L
 
 

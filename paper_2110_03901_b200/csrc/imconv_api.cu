@@ -21,6 +21,7 @@
 #include "conv_kernel.cuh"
 #include "conv_halo.cuh"
 #include "conv_rowband.cuh"
+#include "lru.h"
 
 namespace imconv {
 namespace {
@@ -519,9 +520,20 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
 
 using namespace imconv;
 
+int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, imconv_traffic *out);
+
 extern "C" {
 
 int imconv_abi_version(void) { return IMCONV_ABI_VERSION; }
+
+int imconv_predict_traffic(const imconv_conv_args *args, int64_t l2_bytes, int32_t sms, imconv_traffic *out) {
+    if (!args || !out) return IMCONV_EINVAL;
+    try {
+        return predict_traffic_impl(args, l2_bytes, sms, out);
+    } catch (...) {
+        return IMCONV_EINVAL;  // (allocation failure of the replay's bookkeeping)
+    }
+}
 
 int64_t imconv_out_extent(int64_t size, int64_t f, int64_t stride, int64_t pad, int64_t dil) {
     if (stride < 1 || dil < 1 || f < 1 || pad < 0) return 0;
@@ -559,6 +571,282 @@ int64_t imconv_launch_count(void) { return g_launches; }
 void imconv_debug_set_buffer(void *dev_buf) { g_debug_buf = static_cast<long long *>(dev_buf); }
 void imconv_debug_set_flags(int flags) { g_debug_flags = flags; }
 void imconv_reset_launch_count(void) { g_launches = 0; }
+
+}  // extern "C" (the planner below is internal C++)
+
+// Block-shape / raster decisions of the generic kernel, shared by the launcher
+// and the DRAM-traffic predictor (imconv_predict_traffic) so the model replays
+// exactly the schedule that runs.
+struct GenericPlan {
+    int bn, variant, mt, ksub;
+    bool use_pair;
+    int row_bytes, tps, c_chunks, k_subs;  // k_subs: k-subtiles per block
+    long long m_tiles, n_tiles, tiles;
+    int grid;
+    bool b_resident;
+    int sk_split;        // 1 = off
+    long long sk_tail;   // tail tiles split S ways (sk_split > 1)
+};
+
+int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, GenericPlan *g) {
+    const int64_t K = a->k, R = a->r, S = a->s, C = a->c;
+    const int E = elem_bytes(a->in_dtype);
+    const int64_t M = a->n * P * Q;
+    g->bn = pick_bn(a->in_dtype, K, a->tile_n);
+    if (g->bn < 0) return IMCONV_EINVAL;
+    const int bn = g->bn;
+    // (A wave-quantisation chooser over {256x128, 128x256, 128x128, ...} blocks
+    // was measured worse on the stage-5 layers: smaller blocks lose more
+    // per-block efficiency than they gain in wave fill, so BN is fixed by K.)
+    // 1x1 layers with N = 128: one m-tile per CTA and two k-subtiles per stage measured
+    // faster than two m-tiles (s3 1x1a: 102.5 -> 94.0 us, 44.8 -> 43.7 us); 3x3 and N = 64 lose.
+    const bool no_override = !(a->flags & (IMCONV_FLAG_KSUB1 | IMCONV_FLAG_MT1));
+    const int auto_variant = (no_override && R * S == 1 && bn == 128) ? 1 : -1;
+    // ---- block shape: single CTA or CTA pair (cta_group::2, B split across the pair) ----
+    // pairs need whole swizzle-atom columns per CTA (BN >= 128 bf16 / 256 int8)
+    // and enough 256-row blocks to fill the clusters.
+    const int64_t m_tiles_ = (M + kBM - 1) / kBM;
+    const int64_t n_tiles_ = (K + bn - 1) / bn;
+    const long long pair_tiles = ((m_tiles_ + 1) / 2) * n_tiles_;
+    const bool pair_ok = (a->in_dtype == IMCONV_I8) ? bn == 256 : bn >= 128;
+    // Measured (tools/run_layer.py --flags 1/2): once the producers issue one
+    // TMA per operand per stage, single CTAs match or beat pairs on the
+    // ResNet-50 shapes, so pairs are opt-in for now.
+    g->use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && (a->flags & IMCONV_FLAG_CTA_PAIR) &&
+                  pair_tiles >= 1;
+    // single-CTA block shape (see dispatch_bn): N <= 128 -> 2 m-tiles per CTA
+    g->variant = auto_variant >= 0 ? auto_variant
+                 : (a->flags & IMCONV_FLAG_KSUB1) ? 2 : (a->flags & IMCONV_FLAG_MT1) ? 1 : 0;
+    g->mt = (!g->use_pair && bn <= 128 && g->variant == 0) ? 2 : 1;
+    g->ksub = (!g->use_pair && g->variant == 1) ? 2 : 1;
+    const int64_t cbytes = C * E;
+    g->row_bytes = cbytes >= 128 ? 128 : static_cast<int>(cbytes);  // 16, 32, 64 or 128
+    if (g->row_bytes != 128 && g->row_bytes != 64 && g->row_bytes != 32 && g->row_bytes != 16) return IMCONV_ECHAN;
+    g->tps = kRowBytes / g->row_bytes;
+    g->c_chunks = g->tps == 1 ? static_cast<int>((cbytes + kRowBytes - 1) / kRowBytes) : 1;
+    g->k_subs = g->tps == 1 ? g->c_chunks * static_cast<int>(R * S) : static_cast<int>((R * S + g->tps - 1) / g->tps);
+    const int rows = kBM * g->mt * (g->use_pair ? 2 : 1);
+    g->m_tiles = (M + rows - 1) / rows;
+    g->n_tiles = (K + bn - 1) / bn;
+    g->tiles = g->m_tiles * g->n_tiles;
+    const bool a_gather = g->row_bytes == 16 && E == 2 && !g->use_pair && g->variant != 1;
+    int grid = a->num_ctas > 0 ? a->num_ctas : sms;
+    // B-stationary (1x1 layers with C*e <= 512 B): every k-subtile of a block fits the
+    // 4-deep B ring, so a CTA that always works on the same output-channel block loads
+    // its filter slice once.  Needs grid % n_tiles == 0 (persistent round-robin over
+    // n-fastest tiles then keeps each CTA on one n-block); allowed to drop <= 4% of SMs.
+    g->b_resident = false;
+    if (!g->use_pair && g->variant != 1 && !a_gather && g->k_subs <= 4 && !(g_debug_flags & kDbgNoBResident)) {
+        int gg = static_cast<int>(std::min<long long>(grid, g->tiles));
+        gg = static_cast<int>(gg / g->n_tiles * g->n_tiles);
+        if (gg >= g->n_tiles && gg * 100 >= 96 * std::min<long long>(grid, g->tiles)) {
+            grid = gg;
+            g->b_resident = true;
+        }
+    }
+    // Split-K tail: when the last wave would be at most half full, each of its
+    // `tail` tiles is split into S k-ranges run by S CTAs (S*tail <= grid); the
+    // partial sums meet in an fp32/int32 workspace and the last split stores.
+    // The full waves stay data-parallel.  (Not with B-stationary: split units
+    // change a CTA's output-channel block.)  Measured: pays only when the tail
+    // wave is a large share of the work (at most two waves) and each tile's
+    // k-loop is long enough to amortise the partial write + reduce (s5 3x3:
+    // 55.5 -> 48.3 us; 5-wave s3 layers lose).
+    g->sk_split = 1;
+    g->sk_tail = 0;
+    if (!g->use_pair && !a_gather && !g->b_resident && !(g_debug_flags & kDbgNoSplitK)) {
+        const int k_st = (g->k_subs + g->ksub - 1) / g->ksub;
+        const long long g0 = grid;
+        const long long tail = g->tiles >= g0 ? g->tiles % g0 : g->tiles;
+        constexpr int kSkMinStages = 36;
+        if (tail > 0 && 2 * tail <= g0 && g->tiles < 2 * g0 && k_st >= kSkMinStages) {
+            const int Sk = static_cast<int>(std::min<long long>({g0 / tail, static_cast<long long>(k_st), 4}));
+            if (Sk >= 2) {
+                g->sk_split = Sk;
+                g->sk_tail = tail;
+                if (g->tiles < g0) grid = static_cast<int>(tail * Sk);
+            }
+        }
+    }
+    if (g->use_pair) {
+        if (grid > 2 * g->tiles) grid = static_cast<int>(2 * g->tiles);
+        if (grid < 2) grid = 2;
+    } else if (g->sk_split == 1 && grid > g->tiles) {
+        grid = static_cast<int>(g->tiles);
+    }
+    g->grid = grid;
+    return 0;
+}
+
+// ---- DRAM-traffic predictor (imconv_predict_traffic) ----
+// Line keys: x, w and y live in disjoint 128-byte-line ranges; an activation
+// line is (((n*H + h)*W + w)*C*e + byte) >> 7 -- batch-aware, unlike the
+// reference's (h, w, c) element keys that count every image's identical
+// stream again.
+int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, imconv_traffic *out) {
+    const int64_t N = a->n, H = a->h, W = a->w_, C = a->c, K = a->k, R = a->r, S = a->s;
+    if (N < 1 || H < 1 || W < 1 || C < 1 || K < 1 || R < 1 || S < 1 || sms < 1 || l2_bytes < 0) return IMCONV_EINVAL;
+    if (a->stride_h < 1 || a->stride_w < 1 || a->dil_h < 1 || a->dil_w < 1 || a->pad_h < 0 || a->pad_w < 0)
+        return IMCONV_EINVAL;
+    const bool f16in = a->in_dtype == IMCONV_BF16 || a->in_dtype == IMCONV_F16;
+    if (!f16in && a->in_dtype != IMCONV_I8) return IMCONV_EDTYPE;
+    const int E = elem_bytes(a->in_dtype);
+    const int EO = (a->out_dtype == IMCONV_F32 || a->out_dtype == IMCONV_I32) ? 4 : 2;
+    if ((C * E) % 16 != 0 || (K * E) % 16 != 0) return IMCONV_ECHAN;
+    const int64_t P = imconv_out_extent(H, R, a->stride_h, a->pad_h, a->dil_h);
+    const int64_t Q = imconv_out_extent(W, S, a->stride_w, a->pad_w, a->dil_w);
+    if (P < 1 || Q < 1) return IMCONV_EINVAL;
+    const int64_t M = N * P * Q;
+    GenericPlan g;
+    const int rc = plan_generic(a, P, Q, sms, &g);
+    if (rc) return rc;
+    if (g.use_pair) return IMCONV_EINVAL;  // (CTA-pair rasters are not modelled)
+    std::memset(out, 0, sizeof(*out));
+    out->bn = g.bn;
+    out->mt = g.mt;
+    out->grid = g.grid;
+    out->k_subtiles = g.k_subs;
+    out->tiles = g.tiles;
+    out->kernel = (C * E == 16 && f16in && !(a->flags & IMCONV_FLAG_GATHER16)) ? 1
+                  : (C * E == 128 && a->stride_h == 1 && a->stride_w == 1 && R * S > 1 &&
+                     !(a->flags & IMCONV_FLAG_NO_HALO) && (K == 64 || K == 128 || K == 256) &&
+                     R * S * K * 128 <= 120 * 1024)
+                      ? 2
+                      : 0;
+    const int64_t x_lines = (N * H * W * C * E + 127) / 128;
+    const int64_t w_lines = (R * S * C * K * E + 127) / 128;
+    const int64_t w_base = x_lines, y_base = x_lines + w_lines;
+    const int64_t cap = l2_bytes / 128;
+    imconv::LineLRU lru(std::max<int64_t>(cap, 1));
+    std::vector<uint8_t> seen(static_cast<size_t>(x_lines + w_lines), 0);
+    int64_t reads = 0, requests = 0, compulsory = 0;
+    auto touch_read = [&](int64_t line) {
+        ++requests;
+        if (!seen[static_cast<size_t>(line)]) {
+            seen[static_cast<size_t>(line)] = 1;
+            ++compulsory;
+        }
+        if (cap <= 0 || !lru.access(line, false)) ++reads;
+    };
+    const int rows_per_tile = kBM * g.mt;
+    const int kbke = kRowBytes / E;  // k-rows (reduction elements) per k-subtile
+    const int rs = static_cast<int>(R * S);
+    // A lines of k-subtile ks of m-tile mt_idx (im2col of rows_per_tile output pixels)
+    auto a_lines = [&](long long m_tile, int ks) {
+        const int64_t m0 = m_tile * rows_per_tile;
+        for (int64_t m = m0; m < std::min<int64_t>(m0 + rows_per_tile, M); ++m) {
+            const int64_t n = m / (P * Q), pq = m - n * P * Q, p = pq / Q, q = pq - p * Q;
+            const int taps = g.tps == 1 ? 1 : g.tps;
+            for (int t = 0; t < taps; ++t) {
+                int tap, chunk;
+                if (g.tps == 1) {
+                    if (a->order == IMCONV_ORDER_FILTER_MAJOR) {
+                        tap = ks / g.c_chunks;
+                        chunk = ks - tap * g.c_chunks;
+                    } else {
+                        chunk = ks / rs;
+                        tap = ks - chunk * rs;
+                    }
+                } else {
+                    tap = ks * g.tps + t;
+                    chunk = 0;
+                    if (tap >= rs) break;
+                }
+                const int64_t r = tap / S, s = tap - r * S;
+                const int64_t h = p * a->stride_h - a->pad_h + r * a->dil_h;
+                const int64_t w = q * a->stride_w - a->pad_w + s * a->dil_w;
+                if (h < 0 || h >= H || w < 0 || w >= W) continue;  // zero fill: no memory access
+                const int64_t byte = ((n * H + h) * W + w) * C * E + static_cast<int64_t>(chunk) * 128;
+                const int64_t bytes = std::min<int64_t>(g.tps == 1 ? 128 : C * E, C * E - chunk * 128);
+                for (int64_t l = byte >> 7; l <= (byte + bytes - 1) >> 7; ++l) touch_read(l);
+            }
+        }
+    };
+    auto b_lines = [&](int n_tile, int ks) {
+        int64_t row0;
+        if (g.tps == 1) {
+            int tap, chunk;
+            if (a->order == IMCONV_ORDER_FILTER_MAJOR) {
+                tap = ks / g.c_chunks;
+                chunk = ks - tap * g.c_chunks;
+            } else {
+                chunk = ks / rs;
+                tap = ks - chunk * rs;
+            }
+            row0 = static_cast<int64_t>(tap) * C + static_cast<int64_t>(chunk) * kbke;
+        } else {
+            row0 = static_cast<int64_t>(ks) * g.tps * C;
+        }
+        const int64_t col0 = static_cast<int64_t>(n_tile) * g.bn;
+        const int64_t cols = std::min<int64_t>(g.bn, K - col0);
+        for (int64_t row = row0; row < std::min<int64_t>(row0 + kbke, R * S * C); ++row) {
+            const int64_t byte = (row * K + col0) * E;
+            for (int64_t l = byte >> 7; l <= (byte + cols * E - 1) >> 7; ++l) touch_read(w_base + l);
+        }
+    };
+    auto y_lines = [&](long long m_tile, int n_tile) {
+        const int64_t m0 = m_tile * rows_per_tile, col0 = static_cast<int64_t>(n_tile) * g.bn;
+        const int64_t cols = std::min<int64_t>(g.bn, K - col0);
+        for (int64_t m = m0; m < std::min<int64_t>(m0 + rows_per_tile, M); ++m) {
+            const int64_t byte = (m * K + col0) * EO;
+            for (int64_t l = byte >> 7; l <= (byte + cols * EO - 1) >> 7; ++l) {
+                ++requests;
+                if (cap > 0) lru.access(y_base + l, true);
+            }
+        }
+    };
+    // persistent round-robin; split-K tail units as in get_unit (conv_kernel.cuh)
+    const long long G = g.grid;
+    const long long full_end = g.sk_split > 1 ? g.tiles - g.sk_tail : g.tiles;
+    const int k_stages = (g.k_subs + g.ksub - 1) / g.ksub;
+    struct U { long long tile; int kb0, kb1; bool last_split; };
+    auto unit = [&](long long ui, U &u) {
+        if (ui < full_end) {
+            u = {ui, 0, k_stages, true};
+            return true;
+        }
+        if (g.sk_split <= 1) return false;
+        const long long v = ui - full_end;
+        if (v >= g.sk_tail * g.sk_split) return false;
+        const int sp = static_cast<int>(v % g.sk_split);
+        u = {full_end + v / g.sk_split, sp * k_stages / g.sk_split, (sp + 1) * k_stages / g.sk_split,
+             sp == g.sk_split - 1};
+        return true;
+    };
+    std::vector<uint8_t> b_loaded(static_cast<size_t>(G), 0);
+    for (long long round = 0;; ++round) {
+        bool any = false;
+        for (int kb = 0; kb < k_stages; ++kb) {
+            for (long long b = 0; b < G; ++b) {
+                U u;
+                if (!unit(b + round * G, u) || kb < u.kb0 || kb >= u.kb1) continue;
+                any = true;
+                const long long m_tile = u.tile / g.n_tiles;
+                const int n_tile = static_cast<int>(u.tile - m_tile * g.n_tiles);
+                for (int sub = 0; sub < g.ksub; ++sub) {
+                    const int ks = kb * g.ksub + sub;
+                    if (ks >= g.k_subs) break;
+                    a_lines(m_tile, ks);
+                    if (!g.b_resident || !b_loaded[static_cast<size_t>(b)]) b_lines(n_tile, ks);
+                }
+                if (kb == u.kb1 - 1) {
+                    if (g.b_resident) b_loaded[static_cast<size_t>(b)] = 1;
+                    if (u.last_split) y_lines(m_tile, n_tile);
+                }
+            }
+        }
+        if (!any) break;
+    }
+    out->dram_read_bytes = reads * 128;
+    out->dram_write_bytes = lru.dirty_evictions() * 128;
+    out->resident_dirty_bytes = cap > 0 ? lru.dirty_resident() * 128 : 0;
+    if (cap <= 0) out->dram_write_bytes = (M * K * EO + 127) / 128 * 128;
+    out->line_requests = requests;
+    out->compulsory_read_bytes = compulsory * 128;
+    return 0;
+}
+
+extern "C" {
 
 int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     if (!a || !a->x || !a->w || !a->y) return IMCONV_EINVAL;
@@ -610,32 +898,11 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         if (hr != kNotApplicable) return hr;
     }
 
-    const int bn = pick_bn(a->in_dtype, K, a->tile_n);
-    if (bn < 0) return IMCONV_EINVAL;
-    // (A wave-quantisation chooser over {256x128, 128x256, 128x128, ...} blocks
-    // was measured worse on the stage-5 layers: smaller blocks lose more
-    // per-block efficiency than they gain in wave fill, so BN is fixed by K.)
-    // 1x1 layers with N = 128: one m-tile per CTA and two k-subtiles per stage measured
-    // faster than two m-tiles (s3 1x1a: 102.5 -> 94.0 us, 44.8 -> 43.7 us); 3x3 and N = 64 lose.
-    const bool no_override = !(a->flags & (IMCONV_FLAG_KSUB1 | IMCONV_FLAG_MT1));
-    const int auto_variant = (no_override && R * S == 1 && bn == 128) ? 1 : -1;
-
-    // ---- block shape: single CTA or CTA pair (cta_group::2, B split across the pair) ----
-    // pairs need whole swizzle-atom columns per CTA (BN >= 128 bf16 / 256 int8)
-    // and enough 256-row blocks to fill the clusters.
-    const int64_t m_tiles_ = (M + kBM - 1) / kBM;
-    const int64_t n_tiles_ = (K + bn - 1) / bn;
-    const long long pair_tiles = ((m_tiles_ + 1) / 2) * n_tiles_;
-    const bool pair_ok = (a->in_dtype == IMCONV_I8) ? bn == 256 : bn >= 128;
-    // Measured (tools/run_layer.py --flags 1/2): once the producers issue one
-    // TMA per operand per stage, single CTAs match or beat pairs on the
-    // ResNet-50 shapes, so pairs are opt-in for now.
-    const bool use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && (a->flags & IMCONV_FLAG_CTA_PAIR) &&
-                          pair_tiles >= 1;
-    // single-CTA block shape (see dispatch_bn): N <= 128 -> 2 m-tiles per CTA
-    const int variant = auto_variant >= 0 ? auto_variant
-                        : (a->flags & IMCONV_FLAG_KSUB1) ? 2 : (a->flags & IMCONV_FLAG_MT1) ? 1 : 0;
-    const int mt = (!use_pair && bn <= 128 && variant == 0) ? 2 : 1;
+    GenericPlan plan;
+    rc = plan_generic(a, P, Q, sms, &plan);
+    if (rc) return rc;
+    const int bn = plan.bn, variant = plan.variant, mt = plan.mt;
+    const bool use_pair = plan.use_pair;
 
     // ---- A operand: im2col tensor map over NHWC ----
     const int64_t cbytes = C * E;
@@ -772,25 +1039,11 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     p.dbg_flags = g_debug_flags & 0xff;
 
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
-    int grid = a->num_ctas > 0 ? a->num_ctas : sms;
+    int grid = plan.grid;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    // B-stationary (1x1 layers with C*e <= 512 B): every k-subtile of a block fits the
-    // 4-deep B ring, so a CTA that always works on the same output-channel block loads
-    // its filter slice once.  Needs grid % n_tiles == 0 (persistent round-robin over
-    // n-fastest tiles then keeps each CTA on one n-block); allowed to drop <= 4% of SMs.
-    if (!use_pair && variant != 1 && !p.a_gather && p.k_stages <= 4 && !(g_debug_flags & kDbgNoBResident)) {
-        int g = static_cast<int>(std::min<long long>(grid, tiles));
-        g = g / p.n_tiles * p.n_tiles;
-        if (g >= p.n_tiles && g * 100 >= 96 * std::min<long long>(grid, tiles)) {
-            grid = g;
-            p.b_resident = 1;
-        }
-    }
-
+    p.b_resident = plan.b_resident ? 1 : 0;
     if (use_pair) {
-        int g2 = grid;
-        if (g2 > 2 * tiles) g2 = static_cast<int>(2 * tiles);
-        if (g2 < 2) g2 = 2;
+        const int g2 = grid;
         switch (a->in_dtype) {
             case IMCONV_BF16:
                 return a->out_dtype == IMCONV_F32 ? dispatch_bn_pair<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
@@ -803,43 +1056,27 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         }
     }
 
-    // Split-K tail: when the last wave would be at most half full, each of its
-    // `tail` tiles is split into S k-ranges run by S CTAs (S*tail <= grid); the
-    // partial sums meet in an fp32/int32 workspace and the last split stores.
-    // The full waves stay data-parallel.  (Not with B-stationary: split units
-    // change a CTA's output-channel block.)
+    // split-K tail (plan_generic): stream-ordered partial-sum workspace + tagged counters
     void *sk_ws = nullptr;
     p.sk_split = 1;
-    if (!use_pair && !p.a_gather && !p.b_resident && !(g_debug_flags & kDbgNoSplitK)) {
-        const int ksub = variant == 1 ? 2 : 1;
-        const int k_st = (p.k_stages + ksub - 1) / ksub;
-        const long long g0 = grid;
-        const long long tail = tiles >= g0 ? tiles % g0 : tiles;
-        // measured: pays only when the tail wave is a large share of the work (at most
-        // two waves) and each tile's k-loop is long enough to amortise the partial
-        // write + reduce (s5 3x3: 55.5 -> 48.3 us; 5-wave s3 layers lose)
-        constexpr int kSkMinStages = 36;
-        if (tail > 0 && 2 * tail <= g0 && tiles < 2 * g0 && k_st >= kSkMinStages) {
-            const int S = static_cast<int>(std::min<long long>({g0 / tail, static_cast<long long>(k_st), 4}));
-            int dev = 0;
-            cudaGetDevice(&dev);
-            unsigned long long *cnt = S >= 2 ? sk_counters(dev) : nullptr;
-            const size_t ws_bytes = static_cast<size_t>(tail) * S * (kBM * mt) * bn * 4;
-            if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
-                const unsigned long long gen = g_sk_gen.fetch_add(1);
-                p.sk_split = S;
-                p.sk_first = tiles - tail;
-                p.sk_ws = static_cast<float *>(sk_ws);
-                p.sk_gen = gen;
-                p.sk_cnt = cnt + (gen % kSkSlices) * kSkSliceLen;
-                if (tiles < g0) grid = static_cast<int>(tail * S);
-            } else {
-                sk_ws = nullptr;
-                cudaGetLastError();  // (allocation failure: run without splitting)
-            }
+    if (plan.sk_split > 1) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        unsigned long long *cnt = sk_counters(dev);
+        const size_t ws_bytes = static_cast<size_t>(plan.sk_tail) * plan.sk_split * (kBM * mt) * bn * 4;
+        if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
+            const unsigned long long gen = g_sk_gen.fetch_add(1);
+            p.sk_split = plan.sk_split;
+            p.sk_first = tiles - plan.sk_tail;
+            p.sk_ws = static_cast<float *>(sk_ws);
+            p.sk_gen = gen;
+            p.sk_cnt = cnt + (gen % kSkSlices) * kSkSliceLen;
+        } else {
+            sk_ws = nullptr;
+            cudaGetLastError();  // (allocation failure: run without splitting)
+            grid = static_cast<int>(std::min<long long>(grid, tiles));
         }
     }
-    if (p.sk_split == 1 && grid > tiles) grid = static_cast<int>(tiles);
     int rc_launch;
     switch (a->in_dtype) {
         case IMCONV_BF16:

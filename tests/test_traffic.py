@@ -1,0 +1,71 @@
+"""DRAM-traffic predictor (host C++ replay of the kernel raster).
+
+CPU tests: the replay runs on the host and needs no GPU.  Measured-vs-predicted
+agreement on B200 is in profiles/r1/traffic_predictor.md (tools/traffic_validate.py).
+"""
+
+import ctypes
+
+import pytest
+
+from paper_2110_03901_b200 import ConvSpec, _lib
+from paper_2110_03901_b200.traffic import predict
+
+
+def _lines(nbytes):
+    return (nbytes + 127) // 128 * 128
+
+
+def test_large_cache_reads_are_compulsory():
+    # 1x1 stride 1: every input and filter byte exactly once; output stays resident
+    sp = ConvSpec.square(4, 64, 28, 128, 1)
+    p = predict(sp, l2_bytes=1 << 30)
+    assert p.dram_read_bytes == p.compulsory_read_bytes
+    assert p.dram_read_bytes == _lines(4 * 28 * 28 * 64 * 2) + _lines(64 * 128 * 2)
+    assert p.dram_write_bytes == 0 and p.resident_dirty_bytes == 4 * 28 * 28 * 128 * 2
+
+
+def test_padding_taps_touch_no_memory():
+    # 3x3 pad 1 on a 1x1 image: only the centre tap reads the single pixel
+    sp = ConvSpec.square(2, 64, 1, 64, 3, stride=1, pad=1)
+    p = predict(sp, l2_bytes=1 << 30)
+    assert p.compulsory_read_bytes == _lines(2 * 64 * 2) + _lines(9 * 64 * 64 * 2)
+
+
+def test_no_cache_reads_every_request():
+    sp = ConvSpec.square(2, 128, 14, 64, 3, stride=1, pad=1)
+    p = predict(sp, l2_bytes=0)
+    y_lines = 2 * 14 * 14 * 64 * 2 // 128
+    assert p.dram_read_bytes == (p.line_requests - y_lines) * 128
+    assert p.dram_write_bytes == 2 * 14 * 14 * 64 * 2
+
+
+def test_reuse_aware_order_never_worse_and_helps_small_caches():
+    """The paper's claim in the replay: channel chunk outer / tap inner re-reads the same
+    input window while it is still cached."""
+    sp = ConvSpec.square(8, 512, 14, 256, 3, stride=1, pad=1)
+    for cap in (1 << 20, 4 << 20, 64 << 20):
+        ra = predict(sp, order="reuse_aware", l2_bytes=cap).dram_read_bytes
+        fm = predict(sp, order="filter_major", l2_bytes=cap).dram_read_bytes
+        assert ra <= fm
+    assert predict(sp, order="reuse_aware", l2_bytes=2 << 20).dram_read_bytes < \
+        predict(sp, order="filter_major", l2_bytes=2 << 20).dram_read_bytes
+
+
+def test_plan_matches_launcher_geometry():
+    sp = ConvSpec.square(256, 256, 14, 1024, 1)  # s4 1x1b: BN 256, 4 channel blocks, B-stationary grid
+    p = predict(sp)
+    assert (p.bn, p.mt, p.kernel) == (256, 1, "generic")
+    assert p.tiles == (256 * 14 * 14 + 127) // 128 * 4
+    assert p.grid % 4 == 0
+    stem = predict(ConvSpec.square(256, 8, 224, 64, 7, stride=2, pad=3))
+    assert stem.kernel == "row-band"
+
+
+def test_invalid_arguments():
+    a = _lib.ImconvArgs()
+    t = _lib.ImconvTraffic()
+    assert _lib.lib.imconv_predict_traffic(None, 1 << 20, 148, ctypes.byref(t)) == -1
+    assert _lib.lib.imconv_predict_traffic(ctypes.byref(a), 1 << 20, 148, ctypes.byref(t)) == -1  # zero extents
+    with pytest.raises(_lib.ImconvError):
+        predict(ConvSpec.square(1, 64, 8, 64, 3), sms=0)
