@@ -17,6 +17,7 @@ from __future__ import annotations
 from enum import Enum
 
 from .core import ConvSpec, Layout, Tensor, _as_filter_hwcn, _as_nhwc, direct_conv, gemm
+from .core import ShapeError
 from .lowering import ColumnOrdering, im2col_explicit, lower_filter
 
 
@@ -25,6 +26,25 @@ class Method(Enum):
     CHANNEL_LAST_IMPLICIT = "cl_implicit"
     EXPLICIT_IM2COL = "explicit"
     GEMM = "gemm"
+
+    @classmethod
+    def parse(cls, name: str) -> "Method":
+        """Method from a name or alias (simulator.py:42-58's spellings)."""
+        key = name.strip().lower().replace("-", "_")
+        aliases = {
+            "cf": cls.CHANNEL_FIRST_IMPLICIT, "channel_first": cls.CHANNEL_FIRST_IMPLICIT,
+            "channel_first_implicit": cls.CHANNEL_FIRST_IMPLICIT, "cf_implicit": cls.CHANNEL_FIRST_IMPLICIT,
+            "cl": cls.CHANNEL_LAST_IMPLICIT, "channel_last": cls.CHANNEL_LAST_IMPLICIT,
+            "channel_last_implicit": cls.CHANNEL_LAST_IMPLICIT, "cl_implicit": cls.CHANNEL_LAST_IMPLICIT,
+            "explicit": cls.EXPLICIT_IM2COL, "explicit_im2col": cls.EXPLICIT_IM2COL,
+            "gemm": cls.GEMM, "plain_gemm": cls.GEMM,
+        }
+        if key not in aliases:
+            raise ShapeError(f"unknown method {name!r}")
+        return aliases[key]
+
+
+Method.PLAIN_GEMM = Method.GEMM  # the reference's member name
 
 
 ALL_METHODS = tuple(Method)
