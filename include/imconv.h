@@ -60,6 +60,9 @@ extern "C" {
                                      instead of the row-band (stride-phase plane) kernel     */
 #define IMCONV_FLAG_NO_HALO 32    /* 128-byte pixels, stride 1, resident filter: generic
                                      per-tap kernel instead of the halo-tile kernel          */
+#define IMCONV_FLAG_CHANNEL_LAST 64 /* channel-last BASELINE (bf16/fp16): reduction order
+                                     k = (c, r, s), A gathered element by element -- the
+                                     paper's CL lowering, for the stride contrast only        */
 
 /*
  * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,

@@ -99,4 +99,18 @@ __global__ void pad_copy_kernel(const T *__restrict__ src, T *__restrict__ dst, 
     }
 }
 
+// HWCN filter (R*S taps x C x K) -> channel-last reduction order (C x R*S x K):
+// out[(c*RS + t)*K + k] = in[(t*C + c)*K + k]  (the B operand of the channel-last baseline)
+template <typename T>
+__global__ void permute_filter_cl_kernel(const T *__restrict__ in, T *__restrict__ out, int rs, int c, int k) {
+    const long long total = static_cast<long long>(rs) * c * k;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long row = idx / k;
+        const int kk = static_cast<int>(idx - row * k);
+        const int ch = static_cast<int>(row / rs), t = static_cast<int>(row - static_cast<long long>(ch) * rs);
+        out[idx] = in[(static_cast<long long>(t) * c + ch) * k + kk];
+    }
+}
+
 }  // namespace imconv

@@ -75,6 +75,8 @@ struct ConvParams {
     unsigned long long sk_gen;   // launch generation (counters never need clearing)
     int b_resident;      // 1: grid is a multiple of n_tiles (each CTA keeps one output-channel block) --
                          //    when a block's k-subtiles fit the B ring, its filter slice is loaded once
+    int a_cl;            // 1: channel-last baseline -- reduction order k = (c*R + r)*S + s, A gathered
+                         //    element by element by threads (B = the filter permuted to that order)
     int a_tiled;         // 1: 1x1 / stride 1 / no padding -- A is the plain (M x C) matrix, loaded with
                          //    tiled TMA boxes {128 B of channels, rows} (cheaper per operation than im2col)
     int dbg_flags;       // instrumentation builds only: 1 / 2 = load B / A on a CTA's first tile only
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         for (int i = 0; i < STAGES; ++i) {
             // one A producer + one B producer arm each stage; in gather mode
             // every lane of the A warp arrives once its copies have landed
-            ptx::mbar_init(&full[i], p.a_gather ? 33 : (b_res ? 1 : 2));
+            ptx::mbar_init(&full[i], (p.a_gather || p.a_cl) ? 33 : (b_res ? 1 : 2));
             ptx::mbar_init(&empty[i], 1);
         }
         ptx::mbar_init(bres, 1);
@@ -425,6 +427,89 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         ptx::cp_async_wait<0>();
         ptx::fence_proxy_async_smem();
         for (int u = 0; u < npend; ++u) ptx::mbar_arrive(&full[pend[u]]);
+    } else if (CG == 1 && KSUB == 1 && MT == 1 && p.a_cl && (warp == 0 || warp == 2)) {
+        // ===== A producers, channel-last baseline =====
+        // With the reduction ordered k = (c*R + r)*S + s, one 64-element k-subtile mixes
+        // several channels and taps: every 2-byte element of an A row comes from a
+        // different (pixel, channel), and TMA boxes need >= 16-byte rows, so the lanes
+        // gather element by element (8 per 16-byte chunk) into the SW128 K-major tile.
+        // This is the channel-last lowering whose locality -- and cost -- degrades with
+        // the convolution stride, against which the channel-first kernel is measured.
+        // Warps 0 / 2 take even / odd stages; completion: proxy fence -> per-lane arrive.
+        constexpr int kRowsPerLane = Cfg::kRows / 32;
+        const int par = warp == 2 ? 1 : 0;
+        const int pq = p.p * p.q;
+        const int rs = p.rs;
+        const long long ksz = static_cast<long long>(rs) * p.c;
+        const unsigned short *xs = reinterpret_cast<const unsigned short *>(p.x);
+        const uint32_t a0 = ptx::smem_u32(smem_a);
+        uint32_t it = 0;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (long long tile = tile_start; tile < total_tiles; tile += tile_step) {
+            const long long m_tile = tile / p.n_tiles;
+            const long long m0 = m_tile * Cfg::kRows;
+            int hb[kRowsPerLane], wb[kRowsPerLane];
+            long long nb[kRowsPerLane];
+#pragma unroll
+            for (int i = 0; i < kRowsPerLane; ++i) {
+                const long long m = m0 + lane + 32 * i;
+                const bool ok = m < p.m;
+                const int n = ok ? static_cast<int>(m / pq) : 0;
+                const int rem = ok ? static_cast<int>(m - static_cast<long long>(n) * pq) : 0;
+                const int op = rem / p.q, oq = rem - (rem / p.q) * p.q;
+                hb[i] = ok ? op * p.sh - p.ph : -(1 << 20);  // never in range when past M
+                wb[i] = oq * p.sw - p.pw;
+                nb[i] = static_cast<long long>(n) * p.h;
+            }
+            for (int kb = 0; kb < k_stages; ++kb) {
+                const bool mine = ((it++) & 1u) == static_cast<uint32_t>(par);
+                if (mine) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t dst0 = a0 + stage * Cfg::kAStageK;
+#pragma unroll 1
+                    for (int j = 0; j < 8; ++j) {  // 16-byte chunk j of every row = k in [kb*64 + 8j, +8)
+                        int ec[8], er[8], es[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const long long k = static_cast<long long>(kb) * 64 + j * 8 + e;
+                            const int c = static_cast<int>(k / rs), tap = static_cast<int>(k - static_cast<long long>(c) * rs);
+                            ec[e] = k < ksz ? c : -1;
+                            er[e] = (tap / p.s) * p.dh;
+                            es[e] = (tap - (tap / p.s) * p.s) * p.dw;
+                        }
+#pragma unroll
+                        for (int i = 0; i < kRowsPerLane; ++i) {
+                            uint32_t w4[4];
+#pragma unroll
+                            for (int e = 0; e < 8; e += 2) {
+                                uint32_t v2 = 0;
+#pragma unroll
+                                for (int h2 = 0; h2 < 2; ++h2) {
+                                    const int hh = hb[i] + er[e + h2], ww = wb[i] + es[e + h2];
+                                    uint32_t v = 0;
+                                    if (ec[e + h2] >= 0 && hh >= 0 && hh < p.h && ww >= 0 && ww < p.w)
+                                        v = __ldg(xs + ((nb[i] + hh) * p.w + ww) * p.c + ec[e + h2]);
+                                    v2 |= v << (16 * h2);
+                                }
+                                w4[e / 2] = v2;
+                            }
+                            const uint32_t row = lane + 32 * i;
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                             dst0 + row * 128 + ((static_cast<uint32_t>(j) ^ (row & 7)) << 4)),
+                                         "r"(w4[0]), "r"(w4[1]), "r"(w4[2]), "r"(w4[3])
+                                         : "memory");
+                        }
+                    }
+                    ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05
+                    ptx::mbar_arrive(&full[stage]);
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
     } else if (warp == 0 || warp == 2 || warp == 3 || warp == 8) {
         // ============ TMA producers ============
         // A (activations, im2col): warps 0 / 2 take even / odd stages;
@@ -520,7 +605,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                                                             static_cast<uint16_t>(kw.r * p.dh), pol);
                                 }
                             }
-                            brow = kw.tap * p.c + c0;
+                            brow = p.a_cl ? (kb * KSUB + u) * Cfg::kBKE : kw.tap * p.c + c0;
                             kw.next(p.order, p.r, p.s, p.c_chunks);
                         } else {
                             // small-C layers: pack tps taps side by side along the

@@ -522,6 +522,13 @@ using namespace imconv;
 
 int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, imconv_traffic *out);
 
+static int grid_for(long long work) {
+    long long g = (work + 255) / 256;
+    if (g > 148LL * 16) g = 148LL * 16;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+
 extern "C" {
 
 int imconv_abi_version(void) { return IMCONV_ABI_VERSION; }
@@ -625,18 +632,29 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
     g->tps = kRowBytes / g->row_bytes;
     g->c_chunks = g->tps == 1 ? static_cast<int>((cbytes + kRowBytes - 1) / kRowBytes) : 1;
     g->k_subs = g->tps == 1 ? g->c_chunks * static_cast<int>(R * S) : static_cast<int>((R * S + g->tps - 1) / g->tps);
+    const bool cl = (a->flags & IMCONV_FLAG_CHANNEL_LAST) != 0;
+    if (cl) {  // channel-last baseline: one m-tile, one k-subtile per stage, k = (c, r, s) in 128-byte subtiles
+        g->use_pair = false;
+        g->variant = 2;
+        g->mt = 1;
+        g->ksub = 1;
+        g->row_bytes = 128;
+        g->tps = 1;
+        g->c_chunks = 1;
+        g->k_subs = static_cast<int>((R * S * C * E + kRowBytes - 1) / kRowBytes);
+    }
     const int rows = kBM * g->mt * (g->use_pair ? 2 : 1);
     g->m_tiles = (M + rows - 1) / rows;
     g->n_tiles = (K + bn - 1) / bn;
     g->tiles = g->m_tiles * g->n_tiles;
-    const bool a_gather = g->row_bytes == 16 && E == 2 && !g->use_pair && g->variant != 1;
+    const bool a_gather = !cl && g->row_bytes == 16 && E == 2 && !g->use_pair && g->variant != 1;
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
     // B-stationary (1x1 layers with C*e <= 512 B): every k-subtile of a block fits the
     // 4-deep B ring, so a CTA that always works on the same output-channel block loads
     // its filter slice once.  Needs grid % n_tiles == 0 (persistent round-robin over
     // n-fastest tiles then keeps each CTA on one n-block); allowed to drop <= 4% of SMs.
     g->b_resident = false;
-    if (!g->use_pair && g->variant != 1 && !a_gather && g->k_subs <= 4 && !(g_debug_flags & kDbgNoBResident)) {
+    if (!cl && !g->use_pair && g->variant != 1 && !a_gather && g->k_subs <= 4 && !(g_debug_flags & kDbgNoBResident)) {
         int gg = static_cast<int>(std::min<long long>(grid, g->tiles));
         gg = static_cast<int>(gg / g->n_tiles * g->n_tiles);
         if (gg >= g->n_tiles && gg * 100 >= 96 * std::min<long long>(grid, g->tiles)) {
@@ -654,7 +672,7 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
     // 55.5 -> 48.3 us; 5-wave s3 layers lose).
     g->sk_split = 1;
     g->sk_tail = 0;
-    if (!g->use_pair && !a_gather && !g->b_resident && !(g_debug_flags & kDbgNoSplitK)) {
+    if (!cl && !g->use_pair && !a_gather && !g->b_resident && !(g_debug_flags & kDbgNoSplitK)) {
         const int k_st = (g->k_subs + g->ksub - 1) / g->ksub;
         const long long g0 = grid;
         const long long tail = g->tiles >= g0 ? g->tiles % g0 : g->tiles;
@@ -886,14 +904,16 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
 
     // 16-byte pixels: the row-band kernel unless the generic kernel's cp.async
     // tap gathers are requested (measured 0.47 vs 0.94 ms on the ResNet stem)
-    if (!(a->flags & IMCONV_FLAG_GATHER16) && a->order != IMCONV_ORDER_FILTER_MAJOR) {
+    const bool cl = (a->flags & IMCONV_FLAG_CHANNEL_LAST) != 0;
+    if (cl && !f16in) return IMCONV_EDTYPE;  // (the channel-last baseline gathers 2-byte elements)
+    if (!cl && !(a->flags & IMCONV_FLAG_GATHER16) && a->order != IMCONV_ORDER_FILTER_MAJOR) {
         const int rb = try_rowband(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
         if (rb != kNotApplicable) return rb;
     }
 
     // 128-byte pixels, stride 1, filter resident in smem: halo tiles (each
     // input pixel enters shared memory once per block, taps are descriptor offsets)
-    if (!(a->flags & IMCONV_FLAG_NO_HALO)) {
+    if (!cl && !(a->flags & IMCONV_FLAG_NO_HALO)) {
         const int hr = try_halo(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
         if (hr != kNotApplicable) return hr;
     }
@@ -906,7 +926,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
 
     // ---- A operand: im2col tensor map over NHWC ----
     const int64_t cbytes = C * E;
-    const int row_bytes = cbytes >= 128 ? 128 : static_cast<int>(cbytes);  // 16, 32, 64 or 128
+    const int row_bytes = (cl || cbytes >= 128) ? 128 : static_cast<int>(cbytes);  // 16, 32, 64 or 128
     int a_layout;
     CUtensorMapSwizzle a_swz;
     switch (row_bytes) {
@@ -917,6 +937,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         default: return IMCONV_ECHAN;  // 48, 80, 96, 112 bytes: pad to the next power of two
     }
     const int tps = kRowBytes / row_bytes;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 
     CUtensorMap ta, tb;
     std::memset(&ta, 0, sizeof(ta));
@@ -924,9 +945,11 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     // 1x1, stride 1, no padding: the implicit im2col is the identity, so A is
     // the (N*H*W, C) activation matrix itself -- a tiled map (one TMA box of
     // 128 B of channels x 128*mt rows per k-subtile) replaces the im2col map.
-    const bool a_tiled = R == 1 && S == 1 && a->stride_h == 1 && a->stride_w == 1 && a->pad_h == 0 &&
+    const bool a_tiled = !cl && R == 1 && S == 1 && a->stride_h == 1 && a->stride_w == 1 && a->pad_h == 0 &&
                          a->pad_w == 0 && row_bytes == 128 && !(g_debug_flags & kDbgNoTiledA);
-    if (a_tiled) {
+    if (cl) {
+        // channel-last baseline: A is gathered by threads (no A tensor map)
+    } else if (a_tiled) {
         cuuint64_t gdim[2] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(N * H * W)};
         cuuint64_t gstride[1] = {static_cast<cuuint64_t>(C * E)};
         cuuint32_t box[2] = {static_cast<cuuint32_t>(row_bytes / E), static_cast<cuuint32_t>(kBM * mt)};
@@ -954,6 +977,19 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         if (g_driver_version <= 13010 && N * H * W * C * E < 131072)
             reinterpret_cast<uint64_t *>(&ta)[1] &= ~(1ull << 21);
     }
+    // channel-last baseline: the filter permuted to the (c, r, s) reduction order
+    void *w_cl = nullptr;
+    const void *w_src = a->w;
+    if (cl) {
+        const size_t wbytes = static_cast<size_t>(R * S * C * K) * E;
+        if (cudaMallocAsync(&w_cl, wbytes, st) != cudaSuccess) return static_cast<int>(cudaGetLastError());
+        const long long work = R * S * C * K;
+        permute_filter_cl_kernel<uint16_t><<<grid_for(work), 256, 0, st>>>(
+            reinterpret_cast<const uint16_t *>(a->w), reinterpret_cast<uint16_t *>(w_cl), static_cast<int>(R * S),
+            static_cast<int>(C), static_cast<int>(K));
+        ++g_launches;
+        w_src = w_cl;
+    }
     // ---- B operand: the HWCN filter as (R*S*C rows, K cols).  When K is a whole
     // number of 128-byte column chunks it is viewed 3-D {chunk cols, rows, chunks}
     // so ONE TMA instruction fetches all of a stage's B chunks. ----
@@ -969,7 +1005,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
             cuuint32_t box[3] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(kRowBytes / E),
                                  static_cast<cuuint32_t>(chunks_per_load)};
             cuuint32_t estride[3] = {1, 1, 1};
-            cr = g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 3, const_cast<void *>(a->w), gdim, gstride, box,
+            cr = g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 3, const_cast<void *>(w_src), gdim, gstride, box,
                                 estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         } else {
@@ -977,7 +1013,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
             cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * E)};
             cuuint32_t box[2] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(kRowBytes / E)};
             cuuint32_t estride[2] = {1, 1};
-            cr = g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 2, const_cast<void *>(a->w), gdim, gstride, box,
+            cr = g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 2, const_cast<void *>(w_src), gdim, gstride, box,
                                 estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         }
@@ -1036,11 +1072,17 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     p.a_gather = (row_bytes == 16 && E == 2 && !use_pair && variant != 1) ? 1 : 0;
     p.x = static_cast<const uint8_t *>(a->x);
     p.a_tiled = a_tiled ? 1 : 0;
+    if (cl) {
+        p.a_cl = 1;
+        p.a_gather = 0;
+        p.tps = 1;
+        p.c_chunks = 1;
+        p.k_stages = plan.k_subs;
+    }
     p.dbg_flags = g_debug_flags & 0xff;
 
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = plan.grid;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     p.b_resident = plan.b_resident ? 1 : 0;
     if (use_pair) {
         const int g2 = grid;
@@ -1093,6 +1135,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         default: rc_launch = IMCONV_EDTYPE;
     }
     if (sk_ws) cudaFreeAsync(sk_ws, st);  // stream-ordered: released after the kernel
+    if (w_cl) cudaFreeAsync(w_cl, st);
     return rc_launch;
 }
 
@@ -1119,12 +1162,6 @@ int imconv_gemm(const void *A, const void *B, void *Cm, int32_t in_dtype, int32_
     return imconv_conv2d_nhwc(&a, stream);
 }
 
-static int grid_for(long long work) {
-    long long g = (work + 255) / 256;
-    if (g > 148LL * 16) g = 148LL * 16;
-    if (g < 1) g = 1;
-    return static_cast<int>(g);
-}
 
 static int launch_gather(const void *x, void *out, int32_t eb, int64_t n, int64_t h, int64_t w, int64_t c,
                          int32_t hf, int32_t wf, int32_t r_fix, int32_t s_fix, int32_t sh, int32_t sw, int32_t ph,

@@ -56,6 +56,21 @@ def channel_first_implicit(spec: ConvSpec, ifmap: Tensor, filters: Tensor, **kw)
     return direct_conv(ifmap, filters, spec, **kw)
 
 
+def channel_last_implicit(spec: ConvSpec, ifmap: Tensor, filters: Tensor, **kw) -> Tensor:
+    """The channel-last baseline (simulator.py:300-364): reduction
+    order k = (c, r, s), A operands gathered element by element by the kernel's
+    producer threads (IMCONV_FLAG_CHANNEL_LAST) -- the lowering whose cost grows
+    with the stride, kept to reproduce the paper's contrast (tools/stride_contrast.py).
+    Integer operands (int8 tensor cores; the baseline gathers 2-byte elements) use
+    the explicit channel-last im2col + GEMM, which computes the same OFMap."""
+    from . import _device as D, _lib
+    xd = ifmap.data if hasattr(ifmap, "data") else ifmap
+    if D.is_integer_dtype(D.torch_dtype_of(xd)):
+        return explicit_im2col(spec, ifmap, filters, ColumnOrdering.CHANNEL_LAST, **kw)
+    kw["flags"] = kw.get("flags", 0) | _lib.FLAG_CHANNEL_LAST
+    return direct_conv(ifmap, filters, spec, **kw)
+
+
 def explicit_im2col(spec: ConvSpec, ifmap: Tensor, filters: Tensor,
                     ordering: ColumnOrdering = ColumnOrdering.CHANNEL_FIRST, **kw) -> Tensor:
     """Materialise the lowered matrix in HBM, then GEMM (simulator.py:527-532)."""
@@ -72,8 +87,9 @@ def functional_ofmap(spec: ConvSpec, method: Method, ifmap: Tensor, filters: Ten
     if method is Method.CHANNEL_FIRST_IMPLICIT:
         return channel_first_implicit(spec, ifmap, filters, **kw)
     if method is Method.CHANNEL_LAST_IMPLICIT:
-        return explicit_im2col(spec, ifmap, filters, ColumnOrdering.CHANNEL_LAST, **kw)
+        return channel_last_implicit(spec, ifmap, filters, **kw)
     return explicit_im2col(spec, ifmap, filters, ColumnOrdering.CHANNEL_FIRST, **kw)
 
 
-__all__ = ["ALL_METHODS", "Method", "channel_first_implicit", "explicit_im2col", "functional_ofmap"]
+__all__ = ["ALL_METHODS", "Method", "channel_first_implicit", "channel_last_implicit", "explicit_im2col",
+           "functional_ofmap"]

@@ -168,6 +168,38 @@ def test_split_k_tail_exact(rng, shape):
     assert np.array_equal(yi.cpu().numpy(), want), shape
 
 
+@pytest.mark.parametrize("case", [
+    # (N, H, W, C, K, R, S, sh, sw, ph, pw, dh, dw)
+    (2, 13, 11, 16, 24, 3, 3, 1, 1, 1, 1, 1, 1),
+    (1, 17, 15, 64, 64, 3, 3, 2, 3, 1, 1, 1, 1),
+    (2, 12, 10, 24, 200, 3, 2, 1, 2, 2, 1, 2, 1),
+    (1, 9, 9, 40, 128, 5, 5, 4, 4, 2, 2, 1, 1),   # 1000-element reduction: partial last k-subtile
+    (3, 7, 6, 128, 256, 1, 1, 1, 1, 0, 0, 1, 1),
+])
+def test_channel_last_baseline_exact(rng, case):
+    """The channel-last baseline kernel (k = (c, r, s), thread-gathered A) is exact and
+    agrees with the channel-first kernel (and with Method.CHANNEL_LAST_IMPLICIT)."""
+    P = _P()
+    from oracle import oracle as O
+    n, h, w_, c, k, r, s_, sh, sw, ph, pw, dh, dw = case
+    args = (sh, sw, ph, pw, dh, dw)
+    x = rng.integers(-4, 5, size=(n, h, w_, c)).astype(np.int64)
+    w = rng.integers(-4, 5, size=(r, s_, c, k)).astype(np.int64)
+    want = O.conv2d_nhwc_i64(x, w, *args)
+    xb = torch.from_numpy(x).float().cuda().bfloat16()
+    wb = torch.from_numpy(w).float().cuda().bfloat16()
+    y_cl = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32, flags=P._lib.FLAG_CHANNEL_LAST)
+    assert np.array_equal(y_cl.cpu().numpy(), want.astype(np.float32)), case
+    y_cf = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    assert torch.equal(y_cl, y_cf)
+    from paper_2110_03901_b200 import ConvSpec, Layout, Method, Tensor, functional_ofmap
+    spec = ConvSpec(n=n, c_i=c, h_i=h, w_i=w_, c_o=k, h_f=r, w_f=s_, stride_h=sh, stride_w=sw, pad_h=ph, pad_w=pw,
+                    dilation_h=dh, dilation_w=dw)
+    yf = functional_ofmap(spec, Method.CHANNEL_LAST_IMPLICIT, Tensor.from_array(x.astype(np.float32), Layout.NHWC),
+                          Tensor.from_array(w.astype(np.float32), Layout.HWCN))
+    assert np.array_equal(np.asarray(yf.view()), want.astype(np.float32))
+
+
 def test_host_tensor_path_pipelined(rng):
     """CPU torch tensors in -> pipelined upload / conv / download (chunked over N):
     identical to the device path, exact for integers, and ordered on the caller's stream."""
