@@ -3,7 +3,7 @@
 
 Default workload (BASELINE.json configs[3], "cfg4"): one step = the 53
 convolution layers of ResNet-50 v1.5 at 224x224, batch 256 sharded evenly
-over the ranks (weak scaling per GPU is N/world), bf16 in / bf16 out, fp32
+over the ranks (strong scaling: the global batch is fixed, each GPU takes 256/N images), bf16 in / bf16 out, fp32
 accumulation, synthetic N(0,1) activations and Kaiming weights.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
@@ -208,7 +208,7 @@ def run_reference_arm(args, layers, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "sample_batch": n_sample, "layers": len(layers)},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                          "sample": f"{args.config} all {len(layers)} layers at batch {n_sample} per step "
@@ -455,7 +455,7 @@ def main(argv=None):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16" if args.config != "cfg5" else "int8", "data": "synthetic",
             "config": {"workload": args.config + (" (ResNet-50 v1.5, 53 convs, 224x224)" if args.config == "cfg4" else ""),
                        "global_batch": layers_full[0].spec.n, "per_gpu_batch": work[0][1].n,
