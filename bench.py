@@ -234,6 +234,9 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--layers-json", default=None, help="write per-layer timings here (rank 0)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="diagnostic (1 process): run rank 0's shard of a W-rank job and report W x its "
+                         "throughput, i.e. what the W-GPU run measures when every rank matches rank 0")
     args = ap.parse_args(argv)
 
     from paper_2110_03901_b200.workloads import baseline_configs
@@ -254,9 +257,14 @@ def main(argv=None):
     peaks, peak_kind = load_peaks()
 
     # ---- per-rank shard of every layer (contiguous images; no collective) ----
+    shard_world = world
+    if args.emulate_world > 1:
+        if world != 1:
+            raise SystemExit("--emulate-world is a single-process diagnostic")
+        shard_world = args.emulate_world
     work = []
     for li, layer in enumerate(layers_full):
-        lo, hi = shard_batch(layer.spec.n, world, rank)
+        lo, hi = shard_batch(layer.spec.n, shard_world, rank)
         sp = layer.spec.with_batch(hi - lo)
         g = torch.Generator(device=dev).manual_seed(1000 + li)
         xs = (sp.n, sp.h_i, sp.w_i, sp.c_i)
@@ -343,6 +351,8 @@ def main(argv=None):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     total_flops = sum(l.spec.flops for l in layers_full)  # all ranks together
+    if shard_world != world:  # emulated: every rank assumed as fast as rank 0
+        total_flops = total_flops_rank * shard_world
     value = total_flops / (ms / 1e3) / 1e12
 
     # ---- per-layer kernel times (separate pass): each layer's `reps` launches
@@ -463,11 +473,12 @@ def main(argv=None):
                        "l2": "inputs larger than L2: every layer has its own buffers, "
                              f"per-step working set {bytes_alg_rank / 1e9:.1f} GB per GPU",
                        "cuda_graph": graph is not None},
-            "pct_of_peak": {"measured_sustained": value / world / dtype_peak,
+            **({"emulated_world": shard_world} if shard_world != world else {}),
+            "pct_of_peak": {"measured_sustained": value / shard_world / dtype_peak,
                             "unit_peak": "int8 TOPS" if dtype_peak == int8_peak else "bf16 TFLOP/s",
-                            "measured_burst": value / world / (dtype_peak if dtype_peak == int8_peak
+                            "measured_burst": value / shard_world / (dtype_peak if dtype_peak == int8_peak
                                                                else peaks.get("bf16_tflops", 1648.9)),
-                            "datasheet": value / world / (4500.0 if dtype_peak == int8_peak else 2250.0)},
+                            "datasheet": value / shard_world / (4500.0 if dtype_peak == int8_peak else 2250.0)},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": dtype_peak, "unit": "TFLOP/s",
                          "frac": achieved / dtype_peak,
                          "traffic": None if traffic is None else traffic / world,

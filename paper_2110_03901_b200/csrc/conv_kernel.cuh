@@ -168,6 +168,23 @@ __device__ __forceinline__ void timed_wait_g(uint64_t *bar, uint32_t parity, lon
 #endif
 }
 
+// Launch timeline (IMCONV_INSTRUMENT builds, CTA 0 only): globaltimer stamps of
+// one launch's phases into dbg[148*20 + 1 + (launch % 64) * 8 + event];
+// dbg[148*20] counts launches.  Events: 0 entry, 1 after griddepcontrol.wait,
+// 2 first operands landed (MMA warp), 3 last MMA commit, 4 first accumulator
+// ready (epilogue), 5 last output store complete, 6 exit.
+__device__ __forceinline__ void tl_stamp(long long *dbg, uint32_t idx, int ev) {
+#if IMCONV_INSTRUMENT
+    if (dbg && blockIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        dbg[148 * 20 + 1 + (idx % 64) * 8 + ev] = static_cast<long long>(t);
+    }
+#else
+    (void)dbg, (void)idx, (void)ev;
+#endif
+}
+
 template <int ELEM>
 struct ElemTraits;
 template <>
@@ -296,8 +313,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     uint64_t *tfull = bars + 2 * STAGES;
     uint64_t *tempty = tfull + 2;
     uint64_t *bres = tempty + 2;  // resident filter slice landed (B-stationary mode)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres + 1);
-    volatile uint32_t *sk_last = tmem_slot + 2;  // split-K: this CTA's split was the last of its tile
+    uint64_t *sk_bar = bres + 1;  // split-K: peers' partial blocks landed in the (idle) operand ring
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sk_bar + 1);
+    volatile uint32_t *tl_slot = tmem_slot + 2;  // instrumentation: this launch's timeline index
 
     // broadcast from lane 0: the role branches are then provably warp-uniform and
     // ptxas keeps the MMA issuer's descriptors on the uniform datapath
@@ -320,6 +338,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     const long long full_end = S > 1 ? p.sk_first : total_tiles;
 
     if (warp == 0 && lane == 0) {
+#if IMCONV_INSTRUMENT
+        if (p.dbg && blockIdx.x == 0) {
+            const uint32_t idx = static_cast<uint32_t>(atomicAdd(reinterpret_cast<unsigned long long *>(p.dbg + 148 * 20), 1ull));
+            *tl_slot = idx;
+            tl_stamp(p.dbg, idx, 0);
+        }
+#endif
         ptx::prefetch_tmap(&tmap_a);
         ptx::prefetch_tmap(&tmap_b);
         ptx::prefetch_tmap(&tmap_y);
@@ -330,6 +355,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             ptx::mbar_init(&empty[i], 1);
         }
         ptx::mbar_init(bres, 1);
+        ptx::mbar_init(sk_bar, 1);
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], 4 * CG);  // one arrival per epilogue warp (of both CTAs)
@@ -349,10 +375,12 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tl_idx = IMCONV_INSTRUMENT ? *tl_slot : 0u;
     // PDL: setup above overlaps the previous kernel's tail; no global memory is
     // touched before every prerequisite grid has completed
     ptx::griddep_launch_dependents();
     ptx::griddep_wait();
+    if (IMCONV_INSTRUMENT && threadIdx.x == 0) tl_stamp(p.dbg, tl_idx, 1);
 
     if (CG == 1 && STAGES >= 4 && p.a_gather && (warp == 0 || warp == 2)) {  // (>= 2 ring slots per gather warp)
         // ===== A producers for 16-byte pixels (bf16 C = 8: the ResNet stem) =====
@@ -713,6 +741,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             const uint32_t d_base = tmem_u + static_cast<uint32_t>(acc * MT * BN);
             for (int kb = wu.kb0; kb < wu.kb1; ++kb) {
                 timed_wait_g(&full[stage], phase, w_full);
+                if (IMCONV_INSTRUMENT && ui == tile_start && kb == wu.kb0 && lane == 0) tl_stamp(p.dbg, tl_idx, 2);
                 ptx::tc_fence_after();
                 {
                     const int nsub = min(KSUB, k_subs - kb * KSUB);
@@ -763,6 +792,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        if (IMCONV_INSTRUMENT && lane == 0) tl_stamp(p.dbg, tl_idx, 3);
         if (IMCONV_INSTRUMENT && p.dbg && lane == 0) {
             p.dbg[blockIdx.x * 8 + 2] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 3] = w_tempty;
@@ -800,6 +830,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
             timed_wait_g(&tfull[acc], acc_phase, w_tfull);
+            if (IMCONV_INSTRUMENT && ui == tile_start && warp == 4 && lane == 0) tl_stamp(p.dbg, tl_idx, 4);
             ptx::tc_fence_after();
             if (wu.split < 0) {
 #pragma unroll 1
@@ -835,65 +866,120 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         ptx::mbar_arrive(&tempty[acc]);
                 }
             } else {
-                // ---- split-K tail unit: raw 32-bit partial sums -> workspace [tile][split][row][BN];
-                // the split that arrives last on the tile's counter adds all S partials and stores ----
+                // ---- split-K unit: raw 32-bit partial sums -> workspace; every split then reduces
+                // the output blocks it owns (block b of the tile: m-tile mt, kOC-column chunk j,
+                // b = mt * (BN / kOC) + j, owned by split b % S) ----
+                // Workspace per tail tile: [split][block][kOC/4 column quads][128 rows][4 words],
+                // so a warp writes 512 contiguous bytes per store and an owner fetches each
+                // peer's block with ONE bulk copy; the reduction reads smem conflict-free.
+                constexpr int kBlocks = MT * (BN / kOC);
+                constexpr uint32_t kBlkWords = kBM * kOC;  // 32 KiB (16-bit out) / 16 KiB (32-bit out)
                 const long long tt = tile - full_end;
                 uint32_t *ws_tile = reinterpret_cast<uint32_t *>(p.sk_ws) + tt * S * (Cfg::kRows * BN);
                 uint32_t *ws_mine = ws_tile + static_cast<long long>(wu.split) * (Cfg::kRows * BN);
+                long long ts[6];
+                ts[0] = IMCONV_INSTRUMENT ? clock64() : 0;
 #pragma unroll 1
-                for (int mt = 0; mt < MT; ++mt) {
-#pragma unroll 1
-                    for (int j = 0; j < BN / 32; ++j) {
-                        uint32_t v[32];
-                        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                                    static_cast<uint32_t>(acc * MT * BN + mt * BN + j * 32),
-                                                v);
-                        ptx::tmem_ld_wait();
-                        uint4 *dst = reinterpret_cast<uint4 *>(ws_mine + static_cast<long long>(mt * kBM + row) * BN +
-                                                               j * 32);
+                for (int b = 0; b < kBlocks; ++b) {
+                    const int mt = b / (BN / kOC), j = b - mt * (BN / kOC);
+                    if (n_tile * BN + j * kOC >= p.k || m_tile * Cfg::kRows + mt * kBM >= p.m) continue;
+                    uint32_t v[kOC];
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                    }
+                    for (int h = 0; h < kOC / 32; ++h)
+                        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                                    static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC + h * 32),
+                                                *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
+                    ptx::tmem_ld_wait();
+                    uint4 *dst = reinterpret_cast<uint4 *>(ws_mine + b * kBlkWords) + row;
+#pragma unroll
+                    for (int q = 0; q < kOC / 4; ++q) dst[q * kBM] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                ts[1] = IMCONV_INSTRUMENT ? clock64() : 0;
                 __threadfence();                      // this thread's partial is visible GPU-wide ...
                 ptx::named_bar_sync(5, 128);          // ... for all four epilogue warps
-                if (warp == 4 && lane == 0) *sk_last = sk_arrive(p.sk_cnt + tt, p.sk_gen, S) ? 1u : 0u;
-                ptx::named_bar_sync(6, 160);          // decision -> epilogue warps and the store warp
-                if (*sk_last) {
-                    __threadfence();
-#pragma unroll 1
-                    for (int mt = 0; mt < MT; ++mt) {
-                        const long long row0 = m_tile * Cfg::kRows + mt * kBM;
-#pragma unroll 1
-                        for (int j = 0; j < BN / kOC; ++j) {
-                            const int col0 = n_tile * BN + j * kOC;
-                            if (col0 >= p.k || row0 >= p.m) continue;
-                            uint32_t v[kOC];
-#pragma unroll
-                            for (int q = 0; q < kOC; ++q) v[q] = 0u;
-                            for (int s2 = 0; s2 < S; ++s2) {
-                                const uint4 *src = reinterpret_cast<const uint4 *>(
-                                    ws_tile + (static_cast<long long>(s2) * Cfg::kRows + mt * kBM + row) * BN + j * kOC);
-#pragma unroll
-                                for (int q = 0; q < kOC / 4; ++q) {
-                                    const uint4 t4 = __ldcg(src + q);
-                                    const uint32_t t[4] = {t4.x, t4.y, t4.z, t4.w};
-#pragma unroll
-                                    for (int e = 0; e < 4; ++e) {
-                                        if constexpr (OUT == OUT_I32)
-                                            v[4 * q + e] += t[e];  // int32 two's complement
-                                        else
-                                            v[4 * q + e] = __float_as_uint(__uint_as_float(v[4 * q + e]) +
-                                                                           __uint_as_float(t[e]));
-                                    }
-                                }
-                            }
-                            stage_chunk(v);
+                ts[2] = IMCONV_INSTRUMENT ? clock64() : 0;
+                if (warp == 4 && lane == 0) {
+                    // arrive, then wait for the tile's other splits (all co-resident: the tail
+                    // units are the last unit of distinct persistent CTAs)
+                    unsigned long long *slot = p.sk_cnt + tt;
+                    if (!sk_arrive(slot, p.sk_gen, S)) {
+                        const long long t0 = clock64();
+                        uint32_t tries = 0;
+                        while (true) {
+                            const unsigned long long c = ptx::ld_acquire_gpu(slot);
+                            if ((c >> 8) == p.sk_gen && static_cast<int>(c & 0xff) >= S) break;
+                            __nanosleep(64);
+                            if ((++tries & 1023u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
                         }
                     }
+                    __threadfence();
+                }
+                ptx::named_bar_sync(6, 160);          // all partials visible -> epilogue warps and the store warp
+                ts[3] = IMCONV_INSTRUMENT ? clock64() : 0;
+                ts[4] = 0;
+                // the operand ring is idle (this tail unit is the CTA's last: its MMAs, hence every
+                // load into the ring, have completed), so it receives the peers' partial blocks
+                const uint32_t ring = ptx::smem_u32(smem_a);
+                constexpr uint32_t kRing = STAGES * (Cfg::kAStageK + Cfg::kBStage);
+                const int per_round = static_cast<int>(kRing / (S * kBlkWords * 4));  // >= 1 (host: S <= 5)
+                uint32_t sk_phase = 0;
+                int b = wu.split;
+                while (b < kBlocks) {
+                    // one round: up to per_round owned blocks, S bulk copies each
+                    int nb = 0, bl[8];
+                    for (int bb = b; bb < kBlocks && nb < per_round && nb < 8; bb += S) {
+                        const int mt = bb / (BN / kOC), j = bb - mt * (BN / kOC);
+                        if (n_tile * BN + j * kOC < p.k && m_tile * Cfg::kRows + mt * kBM < p.m) bl[nb++] = bb;
+                        b = bb + S;
+                    }
+                    if (nb == 0) break;
+                    if (warp == 4 && lane == 0) {
+                        ptx::fence_proxy_async_global();
+                        const uint64_t pol = ptx::policy_evict_first();
+                        ptx::mbar_arrive_expect_tx(sk_bar, static_cast<uint32_t>(nb * S * kBlkWords * 4));
+                        for (int i = 0; i < nb; ++i)
+                            for (int s2 = 0; s2 < S; ++s2)
+                                ptx::bulk_load(ring + (i * S + s2) * (kBlkWords * 4),
+                                               ws_tile + static_cast<long long>(s2) * (Cfg::kRows * BN) + bl[i] * kBlkWords,
+                                               kBlkWords * 4, sk_bar, pol);
+                    }
+                    ptx::mbar_wait(sk_bar, sk_phase);
+                    if (IMCONV_INSTRUMENT && ts[4] == 0) ts[4] = clock64();
+                    sk_phase ^= 1;
+                    for (int i = 0; i < nb; ++i) {
+                        uint32_t v[kOC];
+#pragma unroll
+                        for (int q = 0; q < kOC; ++q) v[q] = 0u;
+                        for (int s2 = 0; s2 < S; ++s2) {  // fixed order: deterministic sums
+                            const uint32_t src = ring + (i * S + s2) * (kBlkWords * 4) + row * 16;
+#pragma unroll
+                            for (int q = 0; q < kOC / 4; ++q) {
+                                uint32_t t[4];
+                                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                             : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3])
+                                             : "r"(src + q * (kBM * 16)));
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    if constexpr (OUT == OUT_I32)
+                                        v[4 * q + e] += t[e];  // int32 two's complement
+                                    else
+                                        v[4 * q + e] = __float_as_uint(__uint_as_float(v[4 * q + e]) +
+                                                                       __uint_as_float(t[e]));
+                                }
+                            }
+                        }
+                        stage_chunk(v);
+                    }
+                    ptx::named_bar_sync(5, 128);  // every thread has read this round's blocks
+                }
+                if (IMCONV_INSTRUMENT && p.dbg && warp == 4 && lane == 0) {
+                    ts[5] = clock64();
+                    for (int i = 0; i < 5; ++i) p.dbg[148 * 12 + blockIdx.x * 8 + i] = ts[i + 1] - ts[i];
+                    p.dbg[148 * 12 + blockIdx.x * 8 + 5] = ts[0] - t_start;
+                    p.dbg[148 * 12 + blockIdx.x * 8 + 6] = wu.split;
                 }
             }
             acc ^= 1;
@@ -918,15 +1004,14 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             const long long tile = wu.tile;
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
-            if (wu.split >= 0) {  // split-K unit: only the last split of the tile stores it
-                ptx::named_bar_sync(6, 160);
-                if (!*sk_last) continue;
-            }
+            // split-K unit: this split stores the blocks it owns (b % S == split)
+            if (wu.split >= 0) ptx::named_bar_sync(6, 160);
             for (int mt = 0; mt < MT; ++mt) {
                 const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;
                 for (int j = 0; j < BN / kOC; ++j) {
                     const int col0 = n_tile * BN + j * kOC;
                     if (col0 >= p.k || row0 >= p.m) continue;
+                    if (wu.split >= 0 && (mt * (BN / kOC) + j) % S != wu.split) continue;
                     const uint32_t b = chunk_ctr & 1;
                     ptx::named_bar_sync(1 + b, 160);  // FULL(b)
                     if (lane == 0) {
@@ -942,6 +1027,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             }
         }
         if (lane == 0) ptx::tma_store_wait<0>();
+        if (IMCONV_INSTRUMENT && lane == 0) tl_stamp(p.dbg, tl_idx, 5);
         __syncwarp();
     }
 
@@ -959,6 +1045,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
         }
     }
+    if (IMCONV_INSTRUMENT && threadIdx.x == 0) tl_stamp(p.dbg, tl_idx, 6);
 }
 
 }  // namespace imconv

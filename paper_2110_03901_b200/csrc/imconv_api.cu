@@ -35,6 +35,7 @@ constexpr int kDbgNoTiledA = 1 << 16;     // 1x1 stride-1 layers keep the im2col
 constexpr int kDbgNoBResident = 1 << 17;  // never load the filter slice once per CTA
 constexpr int kDbgNoPdl = 1 << 18;        // launch without programmatic stream serialization
 constexpr int kDbgNoSplitK = 1 << 19;     // never split the tail wave's k-loops
+constexpr int kDbgPersistWs = 1 << 20;    // experiment: split-K workspace from a per-device buffer
 
 // Split-K arrival counters: one per tail tile, tagged with a launch generation
 // so they never need clearing; each launch uses one of 256 slices (so up to
@@ -662,23 +663,29 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
             g->b_resident = true;
         }
     }
-    // Split-K tail: when the last wave would be at most half full, each of its
-    // `tail` tiles is split into S k-ranges run by S CTAs (S*tail <= grid); the
-    // partial sums meet in an fp32/int32 workspace and the last split stores.
-    // The full waves stay data-parallel.  (Not with B-stationary: split units
-    // change a CTA's output-channel block.)  Measured: pays only when the tail
-    // wave is a large share of the work (at most two waves) and each tile's
-    // k-loop is long enough to amortise the partial write + reduce (s5 3x3:
-    // 55.5 -> 48.3 us; 5-wave s3 layers lose).
+    // Split-K: when the blocks do not fill one wave (small per-GPU batches), or the
+    // last wave would be at most half full, each tail tile's k-loop is split S ways
+    // across otherwise-idle CTAs (S*tail <= grid).  Every split writes its 32-bit
+    // partial sums to a workspace, waits for its peers, and reduces + stores the
+    // output blocks it owns (the reduction is spread over the S splits, with one
+    // bulk copy per peer block).  Full waves stay data-parallel.  (Not with
+    // B-stationary: split units change a CTA's output-channel block.)  Each split
+    // keeps >= 4 pipeline stages; S <= 5 so S peer blocks fit the idle operand ring.
     g->sk_split = 1;
     g->sk_tail = 0;
     if (!cl && !g->use_pair && !a_gather && !g->b_resident && !(g_debug_flags & kDbgNoSplitK)) {
         const int k_st = (g->k_subs + g->ksub - 1) / g->ksub;
         const long long g0 = grid;
         const long long tail = g->tiles >= g0 ? g->tiles % g0 : g->tiles;
-        constexpr int kSkMinStages = 36;
-        if (tail > 0 && 2 * tail <= g0 && g->tiles < 2 * g0 && k_st >= kSkMinStages) {
-            const int Sk = static_cast<int>(std::min<long long>({g0 / tail, static_cast<long long>(k_st), 4}));
+        // Measured (tools/small_n_probe.py): the partials' L2 round trip (write 4 B per
+        // output, fence, peer wait, bulk read back) costs ~5-7k cycles per split, so only
+        // long k-loops gain (3x3 with C >= 256: 36+ stages); 16-32-stage 1x1 layers lose.
+        constexpr int kSkMaxSplit = 5, kSkMinStages = 36;
+        const bool sub_wave = g->tiles < g0 && k_st >= kSkMinStages;
+        const bool short_tail = tail > 0 && 2 * tail <= g0 && g->tiles < 2 * g0 && k_st >= kSkMinStages;
+        if (sub_wave || short_tail) {
+            const int Sk = static_cast<int>(std::min<long long>(
+                {g0 / tail, static_cast<long long>(k_st / 4), kSkMaxSplit}));
             if (Sk >= 2) {
                 g->sk_split = Sk;
                 g->sk_tail = tail;
@@ -1106,7 +1113,17 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         cudaGetDevice(&dev);
         unsigned long long *cnt = sk_counters(dev);
         const size_t ws_bytes = static_cast<size_t>(plan.sk_tail) * plan.sk_split * (kBM * mt) * bn * 4;
-        if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
+        static void *persist[64] = {};
+        if ((g_debug_flags & kDbgPersistWs) && !persist[dev]) cudaMalloc(&persist[dev], 64 << 20);
+        void *pws = (g_debug_flags & kDbgPersistWs) && ws_bytes <= (64u << 20) ? persist[dev] : nullptr;
+        if (pws) {
+            const unsigned long long gen = g_sk_gen.fetch_add(1);
+            p.sk_split = plan.sk_split;
+            p.sk_first = tiles - plan.sk_tail;
+            p.sk_ws = static_cast<float *>(pws);
+            p.sk_gen = gen;
+            p.sk_cnt = cnt + (gen % kSkSlices) * kSkSliceLen;
+        } else if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
             const unsigned long long gen = g_sk_gen.fetch_add(1);
             p.sk_split = plan.sk_split;
             p.sk_first = tiles - plan.sk_tail;

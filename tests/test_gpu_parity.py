@@ -168,6 +168,54 @@ def test_split_k_tail_exact(rng, shape):
     assert np.array_equal(yi.cpu().numpy(), want), shape
 
 
+@pytest.mark.parametrize("shape", [
+    # (N, H, W, C, K, R, stride): blocks below one wave, long k-loops -> every tile split
+    (4, 7, 7, 2048, 512, 1, 1),     # ResNet s5 1x1a at a small shard: BN = 256, S = 5
+    (2, 14, 14, 1024, 128, 1, 1),   # BN = 128, two m-tiles per CTA (4 output blocks per tile)
+    (3, 14, 14, 1024, 320, 1, 2),   # strided 1x1, ragged n-tile (K = 320: clipped blocks)
+    (2, 7, 7, 512, 512, 3, 1),      # 3x3 s5 shape at N = 2
+    (1, 9, 9, 256, 64, 3, 1),       # BN = 64
+])
+def test_split_k_sub_wave_exact(rng, shape):
+    """Split-K below one wave: each split writes its partials, waits for its peers and
+    reduces the output blocks it owns.  Exact on integer-valued bf16 (fp32 and bf16 out:
+    the bf16 result is the fp32 sum rounded once), on int8, and equal to the unsplit
+    kernel."""
+    P = _P()
+    from oracle import oracle as O
+    n, h, w_, c, k, r, st = shape
+    pad = r // 2
+    args = (st, st, pad, pad, 1, 1)
+    x = rng.integers(-2, 3, size=(n, h, w_, c)).astype(np.int64)
+    w = rng.integers(-2, 3, size=(r, r, c, k)).astype(np.int64)
+    want = O.conv2d_nhwc_exact_f64(x, w, *args).astype(np.int64)
+    xb = torch.from_numpy(x).float().cuda().bfloat16()
+    wb = torch.from_numpy(w).float().cuda().bfloat16()
+    y = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), shape
+    yb = P._kernels.conv2d_nhwc(xb, wb, *args)
+    assert torch.equal(yb, y.bfloat16()), shape
+    P._lib.lib.imconv_debug_set_flags(1 << 19)  # split-K off
+    try:
+        y_ref = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    finally:
+        P._lib.lib.imconv_debug_set_flags(0)
+    assert torch.equal(y, y_ref)
+    if c % 128 == 0 and k % 128 == 0:
+        xi = torch.from_numpy(x).to(torch.int8).cuda()
+        wi = torch.from_numpy(w).to(torch.int8).cuda()
+        yi = P._kernels.conv2d_nhwc(xi, wi, *args)
+        assert np.array_equal(yi.cpu().numpy(), want), shape
+    # N(0,1) operands: fp32 oracle within the stated tolerance
+    xf = rng.standard_normal((n, h, w_, c)).astype(np.float32)
+    wf = (rng.standard_normal((r, r, c, k)) * (2.0 / (c * r * r)) ** 0.5).astype(np.float32)
+    xq = torch.from_numpy(xf).bfloat16()
+    wq = torch.from_numpy(wf).bfloat16()
+    yq = P._kernels.conv2d_nhwc(xq.cuda(), wq.cuda(), *args, out_dtype=torch.float32).cpu().numpy()
+    ref = O.conv2d_nhwc_taps(xq.float().numpy(), wq.float().numpy(), *args)
+    assert np.abs(yq - ref).max() / max(np.abs(ref).max(), 1e-6) <= 1e-2
+
+
 @pytest.mark.parametrize("case", [
     # (N, H, W, C, K, R, S, sh, sw, ph, pw, dh, dw)
     (2, 13, 11, 16, 24, 3, 3, 1, 1, 1, 1, 1, 1),

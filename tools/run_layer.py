@@ -85,7 +85,7 @@ def run_one(args, layer):
     ms = ev[0].elapsed_time(ev[1]) / args.reps
     print(f"{layer.name} n={sp.n}: {ms:.4f} ms  {sp.flops / ms / 1e9:.1f} TFLOP/s")
     if args.waits:
-        dbg = torch.zeros(148 * 12, dtype=torch.int64, device=dev)
+        dbg = torch.zeros(148 * 20, dtype=torch.int64, device=dev)
         _lib.lib.imconv_debug_set_buffer(dbg.data_ptr())
         conv_device(x, w, *sp.conv_args(), tile_n=args.tile_n, order=order)
         torch.cuda.synchronize()
@@ -94,7 +94,13 @@ def run_one(args, layer):
         names = ["prod_total", "prod_wait_empty", "mma_total", "mma_wait_tempty", "mma_wait_full",
                  "epi_total", "epi_wait_tfull", "epi_tmem_ld"]
         print("  ".join(f"{nm}={v / 1e3:.1f}k" for nm, v in zip(names, d)))
-        e = dbg[148 * 8:].view(148, 4).double().mean(0).tolist()
+        e = dbg[148 * 8:148 * 12].view(148, 4).double().mean(0).tolist()
+        sk = dbg[148 * 12:].view(148, 8)
+        if int(sk[:, 5].abs().sum()) > 0:
+            used = sk[sk[:, 5] != 0].double()
+            print(f"  split-K units ({used.shape[0]} CTAs, cycles, mean/max): " + "  ".join(
+                f"{nm}={used[:, i].mean() / 1e3:.2f}k/{used[:, i].max() / 1e3:.2f}k" for i, nm in enumerate(
+                    ["write_partials", "fence+bar", "arrive+spin", "bulk_wait", "reduce+stage", "start->tfull"])))
         print("  extra (generic: epi barriers+store waits, epi staging; row-band: issuer commit, issuer mma loop, "
               "producer fence+arrive, producer wait_group): " + "  ".join(f"{v / 1e3:.1f}k" for v in e))
 
