@@ -596,11 +596,14 @@ struct GenericPlan {
     long long sk_tail;   // tail tiles split S ways (sk_split > 1)
 };
 
-int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, GenericPlan *g) {
+// One candidate block shape: bn output channels, variant_force >= 0 overrides
+// the m-tile / k-subtile variant (see dispatch_bn).
+int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, int bn_req, int variant_force,
+                    GenericPlan *g) {
     const int64_t K = a->k, R = a->r, S = a->s, C = a->c;
     const int E = elem_bytes(a->in_dtype);
     const int64_t M = a->n * P * Q;
-    g->bn = pick_bn(a->in_dtype, K, a->tile_n);
+    g->bn = pick_bn(a->in_dtype, K, bn_req);
     if (g->bn < 0) return IMCONV_EINVAL;
     const int bn = g->bn;
     // (A wave-quantisation chooser over {256x128, 128x256, 128x128, ...} blocks
@@ -623,7 +626,8 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
     g->use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && (a->flags & IMCONV_FLAG_CTA_PAIR) &&
                   pair_tiles >= 1;
     // single-CTA block shape (see dispatch_bn): N <= 128 -> 2 m-tiles per CTA
-    g->variant = auto_variant >= 0 ? auto_variant
+    g->variant = variant_force >= 0 ? variant_force
+                 : auto_variant >= 0 ? auto_variant
                  : (a->flags & IMCONV_FLAG_KSUB1) ? 2 : (a->flags & IMCONV_FLAG_MT1) ? 1 : 0;
     g->mt = (!g->use_pair && bn <= 128 && g->variant == 0) ? 2 : 1;
     g->ksub = (!g->use_pair && g->variant == 1) ? 2 : 1;
@@ -700,6 +704,35 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
         grid = static_cast<int>(g->tiles);
     }
     g->grid = grid;
+    return 0;
+}
+
+// Block-shape choice.  BN follows K (<= 256); but when the 128 x 256 blocks do
+// not fill one wave (small per-GPU batches: the stage-4/5 layers at N = 32),
+// 128 x 128 blocks with two k-subtiles per stage (twice the blocks, half the
+// tensor work per stage) are compared against 128 x 256 (+ split-K) with a
+// per-CTA latency model: ceil(units / grid) * (stages per unit * cycles per
+// stage + split-K partial round trip).  Measured (tools/small_n_probe.py,
+// N = 32): s4 1x1a 9.7 -> 8.0 us, s5 1x1a 14.5 -> 12.1, s4 3x3 16.3 -> 13.2;
+// s5 3x3 keeps 128 x 256 with a 5-way split (18.0 vs 19.4).
+int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, GenericPlan *g) {
+    int rc = plan_generic_bn(a, P, Q, sms, a->tile_n, -1, g);
+    if (rc || a->tile_n != 0 || g->bn != 256 || g->use_pair || (a->flags & (IMCONV_FLAG_CHANNEL_LAST |
+                                                                             IMCONV_FLAG_KSUB1 | IMCONV_FLAG_MT1)))
+        return rc;
+    if (g->tiles >= sms) return 0;
+    GenericPlan h;
+    if (plan_generic_bn(a, P, Q, sms, 128, 1, &h) != 0 || h.use_pair) return 0;
+    auto cost = [&](const GenericPlan &q, double cyc_stage) {
+        const long long k_st = (q.k_subs + q.ksub - 1) / q.ksub;
+        const long long units = q.sk_split > 1 ? (q.tiles - q.sk_tail) + q.sk_tail * q.sk_split : q.tiles;
+        const long long waves = (units + q.grid - 1) / q.grid;
+        const double per = static_cast<double>(k_st) / q.sk_split * cyc_stage + (q.sk_split > 1 ? 6000.0 : 0.0);
+        return static_cast<double>(waves) * per;
+    };
+    // cycles per pipeline stage in this latency-bound regime (measured ~600 for
+    // 128 x 256 x 64; a 2-k-subtile 128 x 128 stage carries the same tensor work)
+    if (cost(h, 600.0) < cost(*g, 600.0)) *g = h;
     return 0;
 }
 
