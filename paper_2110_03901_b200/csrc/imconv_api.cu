@@ -36,6 +36,7 @@ constexpr int kDbgNoBResident = 1 << 17;  // never load the filter slice once pe
 constexpr int kDbgNoPdl = 1 << 18;        // launch without programmatic stream serialization
 constexpr int kDbgNoSplitK = 1 << 19;     // never split the tail wave's k-loops
 constexpr int kDbgPersistWs = 1 << 20;    // experiment: split-K workspace from a per-device buffer
+constexpr int kDbgNoAutoPair = 1 << 21;   // never pick CTA pairs automatically
 
 // Split-K arrival counters: one per tail tile, tagged with a launch generation
 // so they never need clearing; each launch uses one of 256 slices (so up to
@@ -599,7 +600,7 @@ struct GenericPlan {
 // One candidate block shape: bn output channels, variant_force >= 0 overrides
 // the m-tile / k-subtile variant (see dispatch_bn).
 int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, int bn_req, int variant_force,
-                    GenericPlan *g) {
+                    GenericPlan *g, bool pair_force = false) {
     const int64_t K = a->k, R = a->r, S = a->s, C = a->c;
     const int E = elem_bytes(a->in_dtype);
     const int64_t M = a->n * P * Q;
@@ -623,8 +624,8 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
     // Measured (tools/run_layer.py --flags 1/2): once the producers issue one
     // TMA per operand per stage, single CTAs match or beat pairs on the
     // ResNet-50 shapes, so pairs are opt-in for now.
-    g->use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && (a->flags & IMCONV_FLAG_CTA_PAIR) &&
-                  pair_tiles >= 1;
+    g->use_pair = pair_ok && !(a->flags & IMCONV_FLAG_SINGLE_CTA) &&
+                  ((a->flags & IMCONV_FLAG_CTA_PAIR) || pair_force) && pair_tiles >= 1;
     // single-CTA block shape (see dispatch_bn): N <= 128 -> 2 m-tiles per CTA
     g->variant = variant_force >= 0 ? variant_force
                  : auto_variant >= 0 ? auto_variant
@@ -720,7 +721,19 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
     if (rc || a->tile_n != 0 || g->bn != 256 || g->use_pair || (a->flags & (IMCONV_FLAG_CHANNEL_LAST |
                                                                              IMCONV_FLAG_KSUB1 | IMCONV_FLAG_MT1)))
         return rc;
-    if (g->tiles >= sms) return 0;
+    if (g->tiles >= sms) {
+        // At least one wave of 128 x 256 blocks with the filter streamed (not B-stationary,
+        // no split-K tail): CTA pairs (cta_group::2, 256 x 256 per pair, each CTA loads
+        // half of B) cut the per-SM operand bytes per stage by a third and run a 6-deep
+        // ring.  Measured N = 256: s4 1x1a 29.4 -> 26.6 us, s4 proj 51.7 -> 46.3,
+        // s5 1x1b 25.7 -> 23.9, s4 3x3 42.2 -> 40.7; B-stationary and split-K layers lose.
+        if (!g->b_resident && g->sk_split == 1 && !(a->flags & IMCONV_FLAG_SINGLE_CTA) &&
+            !(g_debug_flags & kDbgNoAutoPair)) {
+            GenericPlan h;
+            if (plan_generic_bn(a, P, Q, sms, 256, -1, &h, true) == 0 && h.use_pair) *g = h;
+        }
+        return 0;
+    }
     GenericPlan h;
     if (plan_generic_bn(a, P, Q, sms, 128, 1, &h) != 0 || h.use_pair) return 0;
     auto cost = [&](const GenericPlan &q, double cyc_stage) {
@@ -758,7 +771,6 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
     GenericPlan g;
     const int rc = plan_generic(a, P, Q, sms, &g);
     if (rc) return rc;
-    if (g.use_pair) return IMCONV_EINVAL;  // (CTA-pair rasters are not modelled)
     std::memset(out, 0, sizeof(*out));
     out->bn = g.bn;
     out->mt = g.mt;
@@ -786,7 +798,8 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
         }
         if (cap <= 0 || !lru.access(line, false)) ++reads;
     };
-    const int rows_per_tile = kBM * g.mt;
+    // a CTA pair is one 256-row unit: each CTA loads its 128 rows of A and half of B
+    const int rows_per_tile = kBM * g.mt * (g.use_pair ? 2 : 1);
     const int kbke = kRowBytes / E;  // k-rows (reduction elements) per k-subtile
     const int rs = static_cast<int>(R * S);
     // A lines of k-subtile ks of m-tile mt_idx (im2col of rows_per_tile output pixels)
@@ -854,7 +867,7 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
         }
     };
     // persistent round-robin; split-K tail units as in get_unit (conv_kernel.cuh)
-    const long long G = g.grid;
+    const long long G = g.use_pair ? g.grid / 2 : g.grid;
     const long long full_end = g.sk_split > 1 ? g.tiles - g.sk_tail : g.tiles;
     const int k_stages = (g.k_subs + g.ksub - 1) / g.ksub;
     struct U { long long tile; int kb0, kb1; bool last_split; };
