@@ -57,6 +57,8 @@ struct RowbandParams {
     int pair_lbo[kMaxPairs];    // byte distance to the second tap's run (> 0)
     int pair_s0[kMaxPairs];     // tap index (0..S-1) of the first / second half; -1 = zero tap
     int pair_s1[kMaxPairs];
+    int row_pair_lbo;         // > 0: output rows j, j+1 share one N = 2*BN MMA (B = two filter rows
+                              // sh apart, the second at this byte distance); 0 = off
     const uint8_t *x;         // NHWC input, 16 bytes per pixel
     long long *dbg;           // optional per-CTA wait-cycle counters (instrumentation), else nullptr
     int dbg_flags;            // instrumentation: 1 = epilogue skips TMEM/stores, 2 = producer skips copies,
@@ -153,7 +155,9 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                     for (int half = 0; half < 2; ++half) {
                         const int s = half ? p.pair_s1[pr] : p.pair_s0[pr];
                         const int row = s >= 0 ? (r * p.s + s) * 8 : rsc;  // rsc: out of range -> zeros
-                        const int grp = (r * p.npairs + pr) * 2 + half;
+                        // filter rows stored in DESCENDING order, so filter row r - sh (the
+                        // next output row's) sits a positive descriptor LBO after row r
+                        const int grp = ((p.r - 1 - r) * p.npairs + pr) * 2 + half;
                         for (int j = 0; j < Cfg::kNChunks; ++j)
                             ptx::tma_load_2d(smem_b + j * p.b_chunk_bytes + grp * 1024, &tmap_w, bfull, j * 64, row,
                                              pol_w);
@@ -304,6 +308,14 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
             adesc_r[k] = ptx::smem_desc(a_base + p.pair_a_off[kk], p.pair_lbo[kk], 128, ptx::LAYOUT_NONE);
         }
         const uint64_t bdesc0 = ptx::smem_desc(b_base, p.b_chunk_bytes, 1024, ptx::LAYOUT_SW128);
+        // Row pairing (BN = 64): input row i feeds output row j through filter row rr and
+        // row j+1 through rr - sh with the SAME A operand, and the two rows' accumulators
+        // are adjacent in TMEM -- so one N = 128 MMA whose B is [W(rr) | W(rr - sh)] (two
+        // 64-column atoms LBO apart) does both: 64 instead of 2 x 48 cycles of A+B reads.
+        const bool row_pairs = BN == 64 && TP >= 2 && p.row_pair_lbo > 0;
+        const uint32_t idesc2 = make_idesc<ELEM, (BN == 64 ? 128 : BN)>();
+        const uint64_t bdesc2 = ptx::smem_desc(b_base, static_cast<uint32_t>(p.row_pair_lbo > 0 ? p.row_pair_lbo : 16),
+                                               1024, ptx::LAYOUT_SW128);
         const uint32_t stage_enc = static_cast<uint32_t>(p.a_stage_bytes >> 4);
         const uint32_t row_enc = static_cast<uint32_t>(p.row_bytes_planes >> 4);
         ptx::mbar_wait(bfull, 0);
@@ -337,11 +349,36 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
 #pragma unroll
                         for (int j = 0; j < TP; ++j) rrs[j] = __shfl_sync(0xffffffffu, rr_tab[i * TP + j], 0);
                     }
+                    bool skip = false;
 #pragma unroll
                     for (int j = 0; j < TP; ++j) {
                         const int rr = rrs[j];
-                        if (rr < 0) continue;  // warp-uniform
-                        const uint64_t b_row = bdesc0 + static_cast<uint64_t>(rr * npairs * 128);
+                        if (skip || rr < 0) {  // warp-uniform
+                            skip = false;
+                            continue;
+                        }
+                        const uint32_t b_off = static_cast<uint32_t>((p.r - 1 - rr) * npairs * 128);
+                        const uint64_t b_row = bdesc0 + b_off;
+                        if (row_pairs && j + 1 < TP && rrs[j + 1] >= 0) {
+                            // rows j and j+1 (filter rows rr and rr - sh >= 0; rr >= sh >= 1)
+                            skip = true;
+                            const int rr1 = rrs[j + 1];
+#pragma unroll
+                            for (int pr = 0; pr < NP; ++pr) {
+                                if (pr >= npairs) continue;
+                                if (pr == 0 && rr1 == 0) {
+                                    // row j+1's first product initialises its accumulator: issue apart
+                                    ptx::mma_f16_elect(d_base + j * BN, adesc_r[pr] + a_add, b_row, idesc, 1u);
+                                    ptx::mma_f16_elect(d_base + (j + 1) * BN, adesc_r[pr] + a_add,
+                                                       bdesc0 + static_cast<uint64_t>((p.r - 1) * npairs * 128),
+                                                       idesc, 0u);
+                                } else {
+                                    ptx::mma_f16_elect(d_base + j * BN, adesc_r[pr] + a_add,
+                                                       bdesc2 + b_off + static_cast<uint64_t>(pr * 128), idesc2, 1u);
+                                }
+                            }
+                            continue;
+                        }
 #pragma unroll
                         for (int pr = 0; pr < NP; ++pr) {
                             if (pr < npairs)

@@ -37,6 +37,7 @@ constexpr int kDbgNoPdl = 1 << 18;        // launch without programmatic stream 
 constexpr int kDbgNoSplitK = 1 << 19;     // never split the tail wave's k-loops
 constexpr int kDbgPersistWs = 1 << 20;    // experiment: split-K workspace from a per-device buffer
 constexpr int kDbgNoAutoPair = 1 << 21;   // never pick CTA pairs automatically
+constexpr int kDbgNoRowPairs = 1 << 22;   // row-band kernel: no N = 128 MMAs over two output rows
 
 // Split-K arrival counters: one per tail tile, tagged with a launch generation
 // so they never need clearing; each launch uses one of 256 slices (so up to
@@ -457,6 +458,11 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
         p.pair_lbo[pr] = s1 >= 0 ? addr[s1] - addr[s0] : 16;  // zero tap: any finite run
     }
     p.n_stages = std::min(24, room / p.a_stage_bytes);
+    // adjacent output rows share N = 128 MMAs (BN = 64, no dilation: filter rows sh apart)
+    p.row_pair_lbo = (BN == 64 && TP >= 2 && p.dh == 1 && !(g_debug_flags & kDbgNoRowPairs))
+                         ? p.sh * p.npairs * 2048 : 0;
+    if (p.row_pair_lbo >= (1 << 18)) p.row_pair_lbo = 0;  // (14-bit LBO field, 16-byte units)
+
     if (p.b_bytes > 128 * 1024 || p.n_stages < 3 || p.in_rows * TP > 256 || 2 * p.n_stages * 8 + 64 > 512 ||
         p.sw * p.needed > kProducers * kMaxEntPerThread)
         return kNotApplicable;

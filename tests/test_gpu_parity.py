@@ -285,6 +285,34 @@ def test_subtile_orders_identical(rng, order):
     assert np.array_equal(y.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("case", [
+    # (N, H, W, K, R, S, sh, sw, ph, pw): 16-byte pixels (C = 8), row-band kernel
+    (2, 40, 38, 64, 7, 7, 2, 2, 3, 3),   # ResNet stem shape: rows paired with filter rows 2 apart
+    (1, 21, 30, 64, 3, 3, 1, 1, 1, 1),   # stride 1: filter rows 1 apart
+    (3, 17, 19, 48, 5, 3, 3, 2, 2, 1),   # stride 3 rows, ragged P (P % 4 != 0), K < 64
+])
+def test_rowband_row_pairs_exact(rng, case):
+    """Row-band kernel: adjacent output rows share N = 128 MMAs (B = two filter rows sh apart,
+    LBO-addressed) -- exact against the oracle and equal to the unpaired kernel."""
+    P = _P()
+    from oracle import oracle as O
+    n, h, w_, k, r, s, sh, sw, ph, pw = case
+    args = (sh, sw, ph, pw, 1, 1)
+    x = rng.integers(-4, 5, size=(n, h, w_, 8)).astype(np.int64)
+    w = rng.integers(-4, 5, size=(r, s, 8, k)).astype(np.int64)
+    want = O.conv2d_nhwc_i64(x, w, *args).astype(np.float32)
+    xb = torch.from_numpy(x).float().cuda().bfloat16()
+    wb = torch.from_numpy(w).float().cuda().bfloat16()
+    y = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    assert np.array_equal(y.cpu().numpy(), want), case
+    P._lib.lib.imconv_debug_set_flags(1 << 22)  # row pairing off
+    try:
+        y_ref = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    finally:
+        P._lib.lib.imconv_debug_set_flags(0)
+    assert torch.equal(y, y_ref)
+
+
 @pytest.mark.parametrize("flags", [0, 8, 16])  # 16-B pixels -> 0: row-band, 8: TMA taps (MT1), 16: cp.async gathers
 def test_small_channel_tap_packing(rng, flags):
     """C*elem < 128 B: several taps share one pipeline stage (16/32/64 B rows)."""
