@@ -18,8 +18,8 @@ FULL_METRICS = [
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", "TMA load bytes (L2->SM)"),
-    ("TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg", "tensor (hmma) active cyc/SM"),
-    ("TPC.TriageCompute.sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg", "tensor (imma) active cyc/SM"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "tensor-core smem operand reads % peak"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % peak"),
     ("gpc__cycles_elapsed.max", "elapsed cycles"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("launch__registers_per_thread", "regs/thread"),
