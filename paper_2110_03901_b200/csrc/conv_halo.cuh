@@ -146,6 +146,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
         const uint64_t adesc0 = ptx::smem_desc(a_base, 16, 1024, ptx::LAYOUT_SW128);
         const uint64_t bdesc0 = ptx::smem_desc(b_base, Cfg::kBChunk, 1024, ptx::LAYOUT_SW128);
+        const uint32_t a_lo0 = static_cast<uint32_t>(adesc0), a_hi = static_cast<uint32_t>(adesc0 >> 32);
+        const uint32_t b_lo0 = static_cast<uint32_t>(bdesc0), b_hi = static_cast<uint32_t>(bdesc0 >> 32);
         ptx::mbar_wait(bfull, 0);
         int stage = 0;
         uint32_t phase = 0;
@@ -157,21 +159,22 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             const uint32_t d = tmem_u + static_cast<uint32_t>(acc * BN);
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            const uint64_t a_st = adesc0 + static_cast<uint64_t>((stage * p.a_stage_bytes) >> 4);
+            // descriptors as (low, high) words: only the start-address field moves
+            const uint32_t a_st = a_lo0 + static_cast<uint32_t>((stage * p.a_stage_bytes) >> 4);
             for (int r = 0; r < p.r; ++r) {
                 for (int s = 0; s < p.s; ++s) {
                     // tap <r,s>: the tile shifted by r*dh rows of QP pixels and s*dw pixels
-                    const uint64_t a_tap = a_st + static_cast<uint64_t>(((r * p.dh) * p.qp + s * p.dw) * 8);
-                    const uint64_t b_tap = bdesc0 + static_cast<uint64_t>(((r * p.s + s) * Cfg::kBTap) >> 4);
+                    const uint32_t a_tap = a_st + static_cast<uint32_t>(((r * p.dh) * p.qp + s * p.dw) * 8);
+                    const uint32_t b_tap = b_lo0 + static_cast<uint32_t>(((r * p.s + s) * Cfg::kBTap) >> 4);
 #pragma unroll
                     for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk) {
                         const uint32_t accum = (r | s | kk) != 0 ? 1u : 0u;
-                        const uint64_t ad = a_tap + static_cast<uint64_t>(kk * 2);  // +32 bytes along K
-                        const uint64_t bd = b_tap + static_cast<uint64_t>((kk * Cfg::kMmaK * kRowBytes) >> 4);
+                        const uint32_t ad = a_tap + static_cast<uint32_t>(kk * 2);  // +32 bytes along K
+                        const uint32_t bd = b_tap + static_cast<uint32_t>((kk * Cfg::kMmaK * kRowBytes) >> 4);
                         if constexpr (ELEM == ELEM_I8)
-                            ptx::mma_i8_elect(d, ad, bd, idesc, accum);
+                            ptx::mma_i8_elect_lh(d, ad, a_hi, bd, b_hi, idesc, accum);
                         else
-                            ptx::mma_f16_elect(d, ad, bd, idesc, accum);
+                            ptx::mma_f16_elect_lh(d, ad, a_hi, bd, b_hi, idesc, accum);
                     }
                 }
             }

@@ -727,6 +727,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         const uint64_t bdesc0 = ptx::smem_desc(__shfl_sync(0xffffffffu, ptx::smem_u32(smem_b), 0),
                                                Cfg::kBKE * kRowBytes, 1024, ptx::LAYOUT_SW128);
         const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
+        const uint32_t a_lo0 = static_cast<uint32_t>(adesc0), a_hi = static_cast<uint32_t>(adesc0 >> 32);
+        const uint32_t b_lo0 = static_cast<uint32_t>(bdesc0), b_hi = static_cast<uint32_t>(bdesc0 >> 32);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -744,30 +746,31 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                 if (IMCONV_INSTRUMENT && ui == tile_start && kb == wu.kb0 && lane == 0) tl_stamp(p.dbg, tl_idx, 2);
                 ptx::tc_fence_after();
                 {
+                    // descriptors as (low, high) words: only the start-address field moves
                     const int nsub = min(KSUB, k_subs - kb * KSUB);
-                    const uint64_t a_st = adesc0 + static_cast<uint64_t>((stage * Cfg::kAStageK) >> 4);
-                    const uint64_t b_st = bdesc0 + static_cast<uint64_t>(((b_res ? kb : stage) * Cfg::kBStage) >> 4);
+                    const uint32_t a_st = a_lo0 + static_cast<uint32_t>((stage * Cfg::kAStageK) >> 4);
+                    const uint32_t b_st = b_lo0 + static_cast<uint32_t>(((b_res ? kb : stage) * Cfg::kBStage) >> 4);
 #pragma unroll
                     for (int u = 0; u < KSUB; ++u) {
                         if (u < nsub) {
 #pragma unroll
                             for (int kk = 0; kk < Cfg::kMmaPerSub; ++kk) {
-                                const uint64_t bdesc =
-                                    b_st + static_cast<uint64_t>((u * Cfg::kBSub + kk * Cfg::kMmaK * kRowBytes) >> 4);
+                                const uint32_t bdesc =
+                                    b_st + static_cast<uint32_t>((u * Cfg::kBSub + kk * Cfg::kMmaK * kRowBytes) >> 4);
                                 const uint32_t accum = (kb != wu.kb0 || (u | kk) != 0) ? 1u : 0u;
 #pragma unroll
                                 for (int mt = 0; mt < MT; ++mt) {
-                                    const uint64_t adesc =
-                                        a_st + static_cast<uint64_t>((u * Cfg::kASub) >> 4) + mt * a_mt + a_kk[kk];
+                                    const uint32_t adesc =
+                                        a_st + static_cast<uint32_t>((u * Cfg::kASub) >> 4) + mt * a_mt + a_kk[kk];
                                     if constexpr (CG == 2) {
                                         if constexpr (ELEM == ELEM_I8)
-                                            ptx::mma_i8_2sm_elect(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                            ptx::mma_i8_2sm_elect_lh(d_base + mt * BN, adesc, a_hi, bdesc, b_hi, idesc, accum);
                                         else
-                                            ptx::mma_f16_2sm_elect(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                            ptx::mma_f16_2sm_elect_lh(d_base + mt * BN, adesc, a_hi, bdesc, b_hi, idesc, accum);
                                     } else if constexpr (ELEM == ELEM_I8) {
-                                        ptx::mma_i8_elect(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                        ptx::mma_i8_elect_lh(d_base + mt * BN, adesc, a_hi, bdesc, b_hi, idesc, accum);
                                     } else {
-                                        ptx::mma_f16_elect(d_base + mt * BN, adesc, bdesc, idesc, accum);
+                                        ptx::mma_f16_elect_lh(d_base + mt * BN, adesc, a_hi, bdesc, b_hi, idesc, accum);
                                     }
                                 }
                             }

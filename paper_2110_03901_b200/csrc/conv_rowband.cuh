@@ -316,6 +316,13 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
         const uint32_t idesc2 = make_idesc<ELEM, (BN == 64 ? 128 : BN)>();
         const uint64_t bdesc2 = ptx::smem_desc(b_base, static_cast<uint32_t>(p.row_pair_lbo > 0 ? p.row_pair_lbo : 16),
                                                1024, ptx::LAYOUT_SW128);
+        // low / high descriptor words (the high words -- SBO, version, layout -- never change)
+        uint32_t a_lo[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) a_lo[k] = static_cast<uint32_t>(adesc_r[k]);
+        const uint32_t a_hi = static_cast<uint32_t>(adesc_r[0] >> 32);
+        const uint32_t b_lo0 = static_cast<uint32_t>(bdesc0), b_lo2 = static_cast<uint32_t>(bdesc2);
+        const uint32_t b_hi = static_cast<uint32_t>(bdesc0 >> 32);
         const uint32_t stage_enc = static_cast<uint32_t>(p.a_stage_bytes >> 4);
         const uint32_t row_enc = static_cast<uint32_t>(p.row_bytes_planes >> 4);
         ptx::mbar_wait(bfull, 0);
@@ -349,6 +356,8 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
 #pragma unroll
                         for (int j = 0; j < TP; ++j) rrs[j] = __shfl_sync(0xffffffffu, rr_tab[i * TP + j], 0);
                     }
+                    // descriptors as (low, high) words: per MMA only the low words move
+                    const uint32_t a_add32 = static_cast<uint32_t>(a_add);
                     bool skip = false;
 #pragma unroll
                     for (int j = 0; j < TP; ++j) {
@@ -358,7 +367,6 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                             continue;
                         }
                         const uint32_t b_off = static_cast<uint32_t>((p.r - 1 - rr) * npairs * 128);
-                        const uint64_t b_row = bdesc0 + b_off;
                         if (row_pairs && j + 1 < TP && rrs[j + 1] >= 0) {
                             // rows j and j+1 (filter rows rr and rr - sh >= 0; rr >= sh >= 1)
                             skip = true;
@@ -368,13 +376,14 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                                 if (pr >= npairs) continue;
                                 if (pr == 0 && rr1 == 0) {
                                     // row j+1's first product initialises its accumulator: issue apart
-                                    ptx::mma_f16_elect(d_base + j * BN, adesc_r[pr] + a_add, b_row, idesc, 1u);
-                                    ptx::mma_f16_elect(d_base + (j + 1) * BN, adesc_r[pr] + a_add,
-                                                       bdesc0 + static_cast<uint64_t>((p.r - 1) * npairs * 128),
-                                                       idesc, 0u);
+                                    ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi, b_lo0 + b_off, b_hi,
+                                                          idesc, 1u);
+                                    ptx::mma_f16_elect_lh(d_base + (j + 1) * BN, a_lo[pr] + a_add32, a_hi,
+                                                          b_lo0 + static_cast<uint32_t>((p.r - 1) * npairs * 128), b_hi,
+                                                          idesc, 0u);
                                 } else {
-                                    ptx::mma_f16_elect(d_base + j * BN, adesc_r[pr] + a_add,
-                                                       bdesc2 + b_off + static_cast<uint64_t>(pr * 128), idesc2, 1u);
+                                    ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi,
+                                                          b_lo2 + b_off + static_cast<uint32_t>(pr * 128), b_hi, idesc2, 1u);
                                 }
                             }
                             continue;
@@ -382,9 +391,9 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
 #pragma unroll
                         for (int pr = 0; pr < NP; ++pr) {
                             if (pr < npairs)
-                                ptx::mma_f16_elect(d_base + j * BN, adesc_r[pr] + a_add,
-                                                   b_row + static_cast<uint64_t>(pr * 128), idesc,
-                                                   (rr | pr) != 0 ? 1u : 0u);
+                                ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi,
+                                                      b_lo0 + b_off + static_cast<uint32_t>(pr * 128), b_hi, idesc,
+                                                      (rr | pr) != 0 ? 1u : 0u);
                         }
                     }
                 }

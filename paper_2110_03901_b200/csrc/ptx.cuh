@@ -375,6 +375,27 @@ __device__ __forceinline__ void mma_f16_elect(uint32_t d_tmem, uint64_t a_desc, 
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Same, with each descriptor passed as (low, high) 32-bit words: callers that only move the
+// start-address field (bits 0-13, no carry into the LBO at 16-29 for shared-memory addresses)
+// keep the high words constant and do one 32-bit add per operand instead of a 64-bit add.
+#define IMCONV_MMA_LH(NAME, INSTR)                                                                           \
+    __device__ __forceinline__ void NAME(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,        \
+                                         uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {                \
+        asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b64 ad, bd;\n\t"                                   \
+                     "mov.b64 ad, {%1, %2};\n\t"                                                           \
+                     "mov.b64 bd, {%3, %4};\n\t"                                                           \
+                     "elect.sync _|e, 0xffffffff;\n\t"                                                     \
+                     "setp.ne.b32 p, %6, 0;\n\t"                                                           \
+                     "@e " INSTR " [%0], ad, bd, %5, p;\n\t}" ::"r"(d_tmem),                               \
+                     "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)                 \
+                     : "memory");                                                                            \
+    }
+IMCONV_MMA_LH(mma_f16_elect_lh, "tcgen05.mma.cta_group::1.kind::f16")
+IMCONV_MMA_LH(mma_i8_elect_lh, "tcgen05.mma.cta_group::1.kind::i8")
+IMCONV_MMA_LH(mma_f16_2sm_elect_lh, "tcgen05.mma.cta_group::2.kind::f16")
+IMCONV_MMA_LH(mma_i8_2sm_elect_lh, "tcgen05.mma.cta_group::2.kind::i8")
+#undef IMCONV_MMA_LH
+
 __device__ __forceinline__ void mma_i8_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                              uint32_t accumulate) {
     asm volatile(
