@@ -509,3 +509,33 @@ def test_cta_pair_parity(rng, flags):
     y = P._kernels.conv2d_nhwc(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), 1, 1, 1, 1, 1, 1,
                                flags=flags)
     assert np.array_equal(y.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("shape", [
+    # (N, H, C, K, R, stride): at least one wave of 128 x 256 blocks with a streamed filter
+    # -> the planner picks CTA pairs on its own (ResNet s4 1x1a / s4 projection / s5 1x1b shapes)
+    (100, 14, 1024, 256, 1, 1),
+    (100, 28, 512, 1024, 1, 2),
+    (60, 7, 512, 2048, 1, 1),
+])
+def test_auto_cta_pairs_exact(rng, shape):
+    """Automatic CTA pairs: exact on integer-valued bf16 (fp32 out), equal to the single-CTA
+    kernel, and within tolerance of the fp32 oracle on N(0,1) operands."""
+    P = _P()
+    from oracle import oracle as O
+    n, h, c, k, r, st = shape
+    args = (st, st, r // 2, r // 2, 1, 1)
+    x = rng.integers(-2, 3, size=(n, h, h, c)).astype(np.int8)
+    w = rng.integers(-2, 3, size=(r, r, c, k)).astype(np.int8)
+    want = O.conv2d_nhwc_exact_f64(x, w, *args)
+    xb = torch.from_numpy(x).cuda().float().bfloat16()
+    wb = torch.from_numpy(w).cuda().float().bfloat16()
+    y = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), shape
+    y1 = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32, flags=P._lib.FLAG_SINGLE_CTA)
+    assert torch.equal(y, y1)
+    xf = torch.randn((n, h, h, c), dtype=torch.float32).bfloat16()
+    wf = (torch.randn((r, r, c, k), dtype=torch.float32) * (2.0 / (c * r * r)) ** 0.5).bfloat16()
+    yq = P._kernels.conv2d_nhwc(xf.cuda(), wf.cuda(), *args).float().cpu().numpy()
+    ref = O.conv2d_nhwc_taps(xf.float().numpy(), wf.float().numpy(), *args)
+    assert _norm_err(yq, ref) <= REL_TOL, shape
