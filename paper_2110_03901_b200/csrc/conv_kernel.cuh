@@ -1029,7 +1029,9 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                 }
             }
         }
-        if (lane == 0) ptx::tma_store_wait<0>();
+        // only the staging reads must finish before exit: the grid's completion (what a
+        // dependent launch waits on) covers the global writes still in flight
+        if (lane == 0) ptx::tma_store_wait_read<0>();
         if (IMCONV_INSTRUMENT && lane == 0) tl_stamp(p.dbg, tl_idx, 5);
         __syncwarp();
     }
