@@ -195,6 +195,13 @@ def cpu_reference_step(layers, n_sample: int, seed: int = 1):
 def run_reference_arm(args, layers, world, rank):
     if rank != 0:
         return 0
+    # torchrun exports OMP_NUM_THREADS=1 to every rank; the reference arm is rank 0 alone,
+    # so it takes all host threads for OpenBLAS
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")
+    except Exception:
+        pass
     n_sample = args.ref_sample
     for _ in range(args.warmup):
         cpu_reference_step(layers[:1], 1)
