@@ -35,7 +35,6 @@ constexpr int kDbgNoTiledA = 1 << 16;     // 1x1 stride-1 layers keep the im2col
 constexpr int kDbgNoBResident = 1 << 17;  // never load the filter slice once per CTA
 constexpr int kDbgNoPdl = 1 << 18;        // launch without programmatic stream serialization
 constexpr int kDbgNoSplitK = 1 << 19;     // never split the tail wave's k-loops
-constexpr int kDbgPersistWs = 1 << 20;    // experiment: split-K workspace from a per-device buffer
 constexpr int kDbgNoAutoPair = 1 << 21;   // never pick CTA pairs automatically
 constexpr int kDbgNoRowPairs = 1 << 22;   // row-band kernel: no N = 128 MMAs over two output rows
 
@@ -1165,17 +1164,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         cudaGetDevice(&dev);
         unsigned long long *cnt = sk_counters(dev);
         const size_t ws_bytes = static_cast<size_t>(plan.sk_tail) * plan.sk_split * (kBM * mt) * bn * 4;
-        static void *persist[64] = {};
-        if ((g_debug_flags & kDbgPersistWs) && !persist[dev]) cudaMalloc(&persist[dev], 64 << 20);
-        void *pws = (g_debug_flags & kDbgPersistWs) && ws_bytes <= (64u << 20) ? persist[dev] : nullptr;
-        if (pws) {
-            const unsigned long long gen = g_sk_gen.fetch_add(1);
-            p.sk_split = plan.sk_split;
-            p.sk_first = tiles - plan.sk_tail;
-            p.sk_ws = static_cast<float *>(pws);
-            p.sk_gen = gen;
-            p.sk_cnt = cnt + (gen % kSkSlices) * kSkSliceLen;
-        } else if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
+        if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
             const unsigned long long gen = g_sk_gen.fetch_add(1);
             p.sk_split = plan.sk_split;
             p.sk_first = tiles - plan.sk_tail;
