@@ -539,3 +539,29 @@ def test_auto_cta_pairs_exact(rng, shape):
     yq = P._kernels.conv2d_nhwc(xf.cuda(), wf.cuda(), *args).float().cpu().numpy()
     ref = O.conv2d_nhwc_taps(xf.float().numpy(), wf.float().numpy(), *args)
     assert _norm_err(yq, ref) <= REL_TOL, shape
+
+
+@pytest.mark.parametrize("case", [
+    # (N, H, C, K, R, stride, pad): one shape per kernel path
+    (2, 30, 8, 64, 7, 2, 3),        # row-band (16-byte pixels), row pairs
+    (2, 20, 64, 64, 3, 1, 1),       # halo tiles (128-byte pixels, stride 1)
+    (2, 21, 128, 200, 3, 2, 1),     # generic TMA-im2col kernel, ragged n-tile
+    (2, 7, 512, 512, 3, 1, 1),      # split-K below one wave
+    (100, 14, 1024, 256, 1, 1, 0),  # automatic CTA pairs
+])
+def test_fp16_paths_exact(rng, case):
+    """fp16 inputs on every kernel path: integer-valued data is exact with fp32 output, and
+    fp16 output equals the fp32 result rounded once."""
+    P = _P()
+    from oracle import oracle as O
+    n, h, c, k, r, st, pad = case
+    args = (st, st, pad, pad, 1, 1)
+    x = rng.integers(-2, 3, size=(n, h, h, c)).astype(np.int8)
+    w = rng.integers(-2, 3, size=(r, r, c, k)).astype(np.int8)
+    want = O.conv2d_nhwc_exact_f64(x, w, *args).astype(np.float32)
+    xh = torch.from_numpy(x).cuda().half()
+    wh = torch.from_numpy(w).cuda().half()
+    y = P._kernels.conv2d_nhwc(xh, wh, *args, out_dtype=torch.float32)
+    assert np.array_equal(y.cpu().numpy(), want), case
+    yh = P._kernels.conv2d_nhwc(xh, wh, *args)
+    assert yh.dtype == torch.float16 and torch.equal(yh, y.half()), case
