@@ -358,44 +358,54 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                     }
                     // descriptors as (low, high) words: per MMA only the low words move
                     const uint32_t a_add32 = static_cast<uint32_t>(a_add);
-                    bool skip = false;
+                    // (the tap-pair loop compiles branch-free when the kernel's NP equals the
+                    // layer's pair count -- the stem -- instead of testing every MMA)
+                    auto issue_row = [&](auto full_c) {
+                        constexpr bool FULL = decltype(full_c)::value;
+                        const int np = FULL ? NP : npairs;
+                        bool skip = false;
 #pragma unroll
-                    for (int j = 0; j < TP; ++j) {
-                        const int rr = rrs[j];
-                        if (skip || rr < 0) {  // warp-uniform
-                            skip = false;
-                            continue;
-                        }
-                        const uint32_t b_off = static_cast<uint32_t>((p.r - 1 - rr) * npairs * 128);
-                        if (row_pairs && j + 1 < TP && rrs[j + 1] >= 0) {
-                            // rows j and j+1 (filter rows rr and rr - sh >= 0; rr >= sh >= 1)
-                            skip = true;
-                            const int rr1 = rrs[j + 1];
+                        for (int j = 0; j < TP; ++j) {
+                            const int rr = rrs[j];
+                            if (skip || rr < 0) {  // warp-uniform
+                                skip = false;
+                                continue;
+                            }
+                            const uint32_t b_off = static_cast<uint32_t>((p.r - 1 - rr) * np * 128);
+                            if (row_pairs && j + 1 < TP && rrs[j + 1] >= 0) {
+                                // rows j and j+1 (filter rows rr and rr - sh >= 0; rr >= sh >= 1)
+                                skip = true;
+                                const int rr1 = rrs[j + 1];
+#pragma unroll
+                                for (int pr = 0; pr < NP; ++pr) {
+                                    if (!FULL && pr >= np) continue;
+                                    if (pr == 0 && rr1 == 0) {
+                                        // row j+1's first product initialises its accumulator: issue apart
+                                        ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi, b_lo0 + b_off, b_hi,
+                                                              idesc, 1u);
+                                        ptx::mma_f16_elect_lh(d_base + (j + 1) * BN, a_lo[pr] + a_add32, a_hi,
+                                                              b_lo0 + static_cast<uint32_t>((p.r - 1) * np * 128), b_hi,
+                                                              idesc, 0u);
+                                    } else {
+                                        ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi,
+                                                              b_lo2 + b_off + static_cast<uint32_t>(pr * 128), b_hi, idesc2, 1u);
+                                    }
+                                }
+                                continue;
+                            }
 #pragma unroll
                             for (int pr = 0; pr < NP; ++pr) {
-                                if (pr >= npairs) continue;
-                                if (pr == 0 && rr1 == 0) {
-                                    // row j+1's first product initialises its accumulator: issue apart
-                                    ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi, b_lo0 + b_off, b_hi,
-                                                          idesc, 1u);
-                                    ptx::mma_f16_elect_lh(d_base + (j + 1) * BN, a_lo[pr] + a_add32, a_hi,
-                                                          b_lo0 + static_cast<uint32_t>((p.r - 1) * npairs * 128), b_hi,
-                                                          idesc, 0u);
-                                } else {
+                                if (FULL || pr < np)
                                     ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi,
-                                                          b_lo2 + b_off + static_cast<uint32_t>(pr * 128), b_hi, idesc2, 1u);
-                                }
+                                                          b_lo0 + b_off + static_cast<uint32_t>(pr * 128), b_hi, idesc,
+                                                          (rr | pr) != 0 ? 1u : 0u);
                             }
-                            continue;
                         }
-#pragma unroll
-                        for (int pr = 0; pr < NP; ++pr) {
-                            if (pr < npairs)
-                                ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi,
-                                                      b_lo0 + b_off + static_cast<uint32_t>(pr * 128), b_hi, idesc,
-                                                      (rr | pr) != 0 ? 1u : 0u);
-                        }
-                    }
+                    };
+                    if (npairs == NP)
+                        issue_row(std::true_type{});
+                    else
+                        issue_row(std::false_type{});
                 }
 #if IMCONV_INSTRUMENT
                 const long long tm1 = clock64();

@@ -5,6 +5,7 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2110_03901_b200/csrc tools/mma_bench.cu -o mma_bench
 #include <cstdio>
+#include <string>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -340,7 +341,20 @@ void run(const char *name) {
     cudaFree(d);
 }
 
-int main() {
+int main(int argc, char **argv) {
+    if (argc > 1 && std::string(argv[1]) == "align") {
+        // no-swizzle K-major A with plane-like LBO (2 KB): 128-B aligned starts vs starts moving by
+        // 16 B (the row-band stem's tap runs)
+        run<64, 6>("SS  none aligned LBO2048");
+        run<64, 5>("SS  none misaligned LBO2048");
+        run<128, 6>("SS  none aligned LBO2048");
+        run<128, 5>("SS  none misaligned LBO2048");
+        run<256, 6>("SS  none aligned LBO2048");
+        run<256, 5>("SS  none misaligned LBO2048");
+        run<64, 0>("SS  A=SW128");
+        run<128, 0>("SS  A=SW128");
+        return 0;
+    }
     // pipe replay of the production issuer (variant 256: uniform datapath), N = 256:
     //   +64 = no full-barrier wait, +1 = no tcgen05 fence -> which part of the per-stage handshake costs
     for (int mps : {4, 8, 16})
