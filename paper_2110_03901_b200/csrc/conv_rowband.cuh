@@ -94,7 +94,11 @@ struct RowbandCfg {
     static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
 };
 
-template <int ELEM, int OUT, int BN, int TP, int NP>
+// STEM = 1: the ResNet-50 stem geometry (7x7, stride 2, dilation 1, 64 channels, 7 input rows per
+// stage, 14 per block) as compile-time constants of the MMA issuer (the host checks the layer matches)
+constexpr int kStemR = 7, kStemSh = 2, kStemRps = 7, kStemInRows = 14;
+
+template <int ELEM, int OUT, int BN, int TP, int NP, int STEM = 0>
 __global__ void __launch_bounds__(kThreadsRowband, 1)
     conv_rowband_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_y,
                         const RowbandParams p) {
@@ -312,7 +316,9 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
         // row j+1 through rr - sh with the SAME A operand, and the two rows' accumulators
         // are adjacent in TMEM -- so one N = 128 MMA whose B is [W(rr) | W(rr - sh)] (two
         // 64-column atoms LBO apart) does both: 64 instead of 2 x 48 cycles of A+B reads.
-        const bool row_pairs = BN == 64 && TP >= 2 && p.row_pair_lbo > 0;
+        const bool row_pairs = BN == 64 && TP >= 2 && (STEM || p.row_pair_lbo > 0);
+        const int g_sh = STEM ? kStemSh : p.sh;  // filter-row step between output rows
+        const int g_r = STEM ? kStemR : p.r;
         const uint32_t idesc2 = make_idesc<ELEM, (BN == 64 ? 128 : BN)>();
         const uint64_t bdesc2 = ptx::smem_desc(b_base, static_cast<uint32_t>(p.row_pair_lbo > 0 ? p.row_pair_lbo : 16),
                                                1024, ptx::LAYOUT_SW128);
@@ -336,21 +342,16 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
             timed_wait(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
             const uint32_t d_base = tmem_u + static_cast<uint32_t>(acc * TP * BN);
-            for (int i0 = 0; i0 < p.in_rows; i0 += p.rps) {
-                timed_wait(&full[stage], phase, w_full);
-                ptx::tc_fence_after();
-#if IMCONV_INSTRUMENT
-                const long long tm0 = clock64();
-#endif
-                for (int ri = 0; ri < p.rps; ++ri) {
-                    const int i = i0 + ri;
+            // one input row i (ri-th of its pipeline stage): every (output row, filter row) pair it
+            // feeds, as MMAs over the stage's planes
+            auto issue_input_row = [&](const int i, const int ri) {
                     const uint64_t a_add = static_cast<uint64_t>(stage * stage_enc + ri * row_enc);
                     int rrs[TP];
-                    if (p.dh == 1) {  // filter row of output row j fed by input row i (no table read)
+                    if (STEM || p.dh == 1) {  // filter row of output row j fed by input row i (no table read)
 #pragma unroll
                         for (int j = 0; j < TP; ++j) {
-                            const int rr = i - j * p.sh;
-                            rrs[j] = (rr >= 0 && rr < p.r) ? rr : -1;
+                            const int rr = i - j * g_sh;
+                            rrs[j] = (rr >= 0 && rr < g_r) ? rr : -1;
                         }
                     } else {
 #pragma unroll
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                                 skip = false;
                                 continue;
                             }
-                            const uint32_t b_off = static_cast<uint32_t>((p.r - 1 - rr) * np * 128);
+                            const uint32_t b_off = static_cast<uint32_t>((g_r - 1 - rr) * np * 128);
                             if (row_pairs && j + 1 < TP && rrs[j + 1] >= 0) {
                                 // rows j and j+1 (filter rows rr and rr - sh >= 0; rr >= sh >= 1)
                                 skip = true;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                                         ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi, b_lo0 + b_off, b_hi,
                                                               idesc, 1u);
                                         ptx::mma_f16_elect_lh(d_base + (j + 1) * BN, a_lo[pr] + a_add32, a_hi,
-                                                              b_lo0 + static_cast<uint32_t>((p.r - 1) * np * 128), b_hi,
+                                                              b_lo0 + static_cast<uint32_t>((g_r - 1) * np * 128), b_hi,
                                                               idesc, 0u);
                                     } else {
                                         ptx::mma_f16_elect_lh(d_base + j * BN, a_lo[pr] + a_add32, a_hi,
@@ -402,11 +403,18 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                             }
                         }
                     };
-                    if (npairs == NP)
+                    if (STEM || npairs == NP)
                         issue_row(std::true_type{});
                     else
                         issue_row(std::false_type{});
-                }
+            };
+            auto issue_stage = [&](auto body) {
+                timed_wait(&full[stage], phase, w_full);
+                ptx::tc_fence_after();
+#if IMCONV_INSTRUMENT
+                const long long tm0 = clock64();
+#endif
+                body();
 #if IMCONV_INSTRUMENT
                 const long long tm1 = clock64();
                 t_loop += tm1 - tm0;
@@ -419,6 +427,21 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                     stage = 0;
                     phase ^= 1;
                 }
+            };
+            if constexpr (STEM) {
+                // the ResNet stem geometry is compile-time (2 stages of 7 input rows): every
+                // (row, filter row, tap pair) decision folds away and the issue is straight-line
+#pragma unroll
+                for (int i0 = 0; i0 < kStemInRows; i0 += kStemRps)
+                    issue_stage([&] {
+#pragma unroll
+                        for (int ri = 0; ri < kStemRps; ++ri) issue_input_row(i0 + ri, ri);
+                    });
+            } else {
+                for (int i0 = 0; i0 < p.in_rows; i0 += p.rps)
+                    issue_stage([&] {
+                        for (int ri = 0; ri < p.rps; ++ri) issue_input_row(i0 + ri, ri);
+                    });
             }
             ptx::mma_commit_elect(&tfull[acc]);
             acc ^= 1;

@@ -37,6 +37,7 @@ constexpr int kDbgNoPdl = 1 << 18;        // launch without programmatic stream 
 constexpr int kDbgNoSplitK = 1 << 19;     // never split the tail wave's k-loops
 constexpr int kDbgNoAutoPair = 1 << 21;   // never pick CTA pairs automatically
 constexpr int kDbgNoRowPairs = 1 << 22;   // row-band kernel: no N = 128 MMAs over two output rows
+constexpr int kDbgNoStemSpec = 1 << 23;   // row-band kernel: no compile-time stem instantiation
 
 // Split-K arrival counters: one per tail tile, tagged with a launch generation
 // so they never need clearing; each launch uses one of 256 slices (so up to
@@ -225,10 +226,10 @@ constexpr int kMaxDynSmem = 227 * 1024;
 
 inline int floordiv(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
 
-template <int ELEM, int OUT, int BN, int TP, int NP>
+template <int ELEM, int OUT, int BN, int TP, int NP, int STEM = 0>
 int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandParams &p, int smem, int grid,
                    cudaStream_t st) {
-    auto kern = conv_rowband_kernel<ELEM, OUT, BN, TP, NP>;
+    auto kern = conv_rowband_kernel<ELEM, OUT, BN, TP, NP, STEM>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
@@ -500,7 +501,11 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
     if (grid > p.tiles) grid = static_cast<int>(p.tiles);
     const bool f32 = a->out_dtype == IMCONV_F32;
+    // the ResNet stem geometry runs an instantiation whose MMA issue is fully compile-time
+    const bool stem = BN == 64 && R == kStemR && S == 7 && p.sh == kStemSh && p.dh == 1 && p.rps == kStemRps &&
+                      p.in_rows == kStemInRows && p.npairs == 4 && p.row_pair_lbo > 0 && !(g_debug_flags & kDbgNoStemSpec);
 #define IMCONV_RB(EL, OUTK)                                                                               \
+    if (stem) return launch_rowband<EL, OUTK, 64, 4, 4, 1>(tw, ty, p, smem, grid, st);                    \
     if (p.npairs <= 4) {                                                                                   \
         switch (BN) {                                                                                      \
             case 64: return launch_rowband<EL, OUTK, 64, 4, 4>(tw, ty, p, smem, grid, st);                 \

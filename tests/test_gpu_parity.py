@@ -288,6 +288,7 @@ def test_subtile_orders_identical(rng, order):
 @pytest.mark.parametrize("case", [
     # (N, H, W, K, R, S, sh, sw, ph, pw): 16-byte pixels (C = 8), row-band kernel
     (2, 40, 38, 64, 7, 7, 2, 2, 3, 3),   # ResNet stem shape: rows paired with filter rows 2 apart
+    (1, 224, 224, 64, 7, 7, 2, 2, 3, 3),  # the stem itself: compile-time issue schedule (STEM instantiation)
     (1, 21, 30, 64, 3, 3, 1, 1, 1, 1),   # stride 1: filter rows 1 apart
     (3, 17, 19, 48, 5, 3, 3, 2, 2, 1),   # stride 3 rows, ragged P (P % 4 != 0), K < 64
 ])
