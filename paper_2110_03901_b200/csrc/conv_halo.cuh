@@ -22,6 +22,12 @@
 // (lowering.py:136-143) becomes descriptor arithmetic, and each input pixel
 // is written to shared memory once per block instead of once per tap.
 //
+// HB = 2 (BN = 64): a block is two such sub-blocks stacked (2*TPR output rows, one input tile of
+// 2*TPR + (R-1)*dh rows).  Sub-block 1's tap <r',s> reads the tile at the same shift as sub-block
+// 0's tap <r'+TPR/dh, s>, and the two accumulators are adjacent in TMEM, so those taps run as ONE
+// N = 128 MMA whose B is [W(r'+TPR/dh, s) | W(r', s)] (two 64-column atoms one LBO apart; the
+// resident filter is stored filter-row-descending): A is read once for both sub-blocks.
+//
 // The filter (R*S taps x 128-byte k-rows x BN) stays resident.  Warp roles as
 // in conv_fwd_kernel: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator,
 // 4-7 = epilogue (TMEM -> swizzled staging of the TPR*Q valid pixels), 9 =
@@ -40,9 +46,9 @@ struct HaloParams {
     int r, s, ph, pw, dh, dw;
     int p, q;
     int qp;                 // padded row pitch of the tile (Q + (S-1)*dw)
-    int tpr;                // output rows per block (floor(128 / qp))
-    int tr;                 // input rows per block (tpr + (R-1)*dh)
-    int p_tiles;            // ceil(P / tpr)
+    int tpr;                // output rows per sub-block (floor(128 / qp))
+    int tr;                 // input rows per block (HB*tpr + (R-1)*dh)
+    int p_tiles;            // ceil(P / (HB*tpr))
     long long tiles;        // n * p_tiles * n_tiles
     int n_tiles;            // output-channel blocks of BN
     int a_stage_bytes;      // tr * qp * 128 rounded up to 1024 (+ slack rows the last taps over-read)
@@ -51,7 +57,7 @@ struct HaloParams {
     int b_bytes;            // resident filter bytes (R*S taps)
 };
 
-template <int ELEM, int OUT, int BN>
+template <int ELEM, int OUT, int BN, int HB = 1>
 struct HaloCfg {
     static constexpr int kE = ElemTraits<ELEM>::kBytes;
     static constexpr int kBKE = kRowBytes / kE;           // k-rows (channels) per tap
@@ -60,17 +66,18 @@ struct HaloCfg {
     static constexpr int kBChunk = kBKE * kRowBytes;      // one column chunk of one tap
     static constexpr int kMmaK = 32 / kE;
     static constexpr int kMmaPerTap = kBKE / kMmaK;       // = 4
-    static constexpr int kTmemCols = 2 * BN;
+    static constexpr int kTmemCols = 2 * HB * BN;
     static constexpr int kOutCols = (OUT == OUT_BF16 || OUT == OUT_F16) ? 64 : 32;
     static constexpr int kOutTile = kBM * 128;
     static_assert(kTmemCols == 128 || kTmemCols == 256 || kTmemCols == 512, "TMEM columns");
 };
 
-template <int ELEM, int OUT, int BN>
+template <int ELEM, int OUT, int BN, int HB = 1>
 __global__ void __launch_bounds__(kThreadsGeneric, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ CUtensorMap tmap_y, const HaloParams p) {
-    using Cfg = HaloCfg<ELEM, OUT, BN>;
+    static_assert(HB == 1 || BN == 64, "stacked sub-blocks share MMAs through one 64-column atom per tap");
+    using Cfg = HaloCfg<ELEM, OUT, BN, HB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *smem_b = smem;                                 // resident filter (1024-aligned size)
@@ -119,7 +126,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             const uint64_t pol_w = ptx::policy_evict_last();
             ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(p.b_bytes));
             // (the resident filter covers all K = BN output channels: n_tiles == 1)
-            for (int t = 0; t < rs; ++t) ptx::tma_load_3d(smem_b + t * Cfg::kBTap, &tmap_b, bfull, 0, t * Cfg::kBKE, 0, pol_w);
+            // tap <r,s> goes to slot (R-1-r)*S + s (filter rows descending: a lower filter row sits
+            // a positive descriptor LBO after a higher one)
+            for (int t = 0; t < rs; ++t) {
+                const int r = t / p.s, s_ = t - r * p.s;
+                ptx::tma_load_3d(smem_b + ((p.r - 1 - r) * p.s + s_) * Cfg::kBTap, &tmap_b, bfull, 0, t * Cfg::kBKE, 0,
+                                 pol_w);
+            }
             // ---- input tiles: one 4-D box {128 B of channels, QP pixels, TR rows, 1 image} ----
             const uint64_t pol_a = ptx::policy_evict_normal();
             int stage = 0;
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 ptx::mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(p.a_box_bytes));
                 ptx::tma_load_4d(smem_a + stage * p.a_stage_bytes, &tmap_a, &full[stage], 0, -p.pw,
-                                 pt * p.tpr - p.ph, n, pol_a);
+                                 pt * (HB * p.tpr) - p.ph, n, pol_a);
                 if (++stage == p.n_stages) {
                     stage = 0;
                     phase ^= 1;
@@ -148,6 +161,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         const uint64_t bdesc0 = ptx::smem_desc(b_base, Cfg::kBChunk, 1024, ptx::LAYOUT_SW128);
         const uint32_t a_lo0 = static_cast<uint32_t>(adesc0), a_hi = static_cast<uint32_t>(adesc0 >> 32);
         const uint32_t b_lo0 = static_cast<uint32_t>(bdesc0), b_hi = static_cast<uint32_t>(bdesc0 >> 32);
+        // stacked sub-blocks (HB = 2): shared taps pair filter rows dr = TPR/dh apart; their B atoms
+        // are dr*S tap slots apart in the row-descending filter (the LBO of the N = 128 descriptor)
+        const int share_dr = (HB == 2 && p.tpr % p.dh == 0 && p.tpr / p.dh < p.r) ? p.tpr / p.dh : 0;
+        const uint64_t bdesc2 = ptx::smem_desc(b_base, static_cast<uint32_t>((share_dr > 0 ? share_dr : 1) * p.s * Cfg::kBTap),
+                                               1024, ptx::LAYOUT_SW128);
+        const uint32_t b_lo2 = static_cast<uint32_t>(bdesc2), b_hi2 = static_cast<uint32_t>(bdesc2 >> 32);
+        const uint32_t idesc2 = make_idesc<ELEM, 2 * BN <= 256 ? 2 * BN : BN>();
         ptx::mbar_wait(bfull, 0);
         int stage = 0;
         uint32_t phase = 0;
@@ -156,27 +176,48 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
             ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
             ptx::tc_fence_after();
-            const uint32_t d = tmem_u + static_cast<uint32_t>(acc * BN);
+            const uint32_t d = tmem_u + static_cast<uint32_t>(acc * HB * BN);
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
             // descriptors as (low, high) words: only the start-address field moves
             const uint32_t a_st = a_lo0 + static_cast<uint32_t>((stage * p.a_stage_bytes) >> 4);
-            for (int r = 0; r < p.r; ++r) {
-                for (int s = 0; s < p.s; ++s) {
-                    // tap <r,s>: the tile shifted by r*dh rows of QP pixels and s*dw pixels
-                    const uint32_t a_tap = a_st + static_cast<uint32_t>(((r * p.dh) * p.qp + s * p.dw) * 8);
-                    const uint32_t b_tap = b_lo0 + static_cast<uint32_t>(((r * p.s + s) * Cfg::kBTap) >> 4);
+            // one tap of one (or both) sub-blocks: A = the tile shifted by `rows` 128-byte rows,
+            // B = the resident filter slot of <r,s> (N = 2*BN over both sub-blocks when `both`)
+            auto tap_mmas = [&](uint32_t d_tap, int rows, int r, int s, bool both, bool first) {
+                const uint32_t a_tap = a_st + static_cast<uint32_t>(rows * 8);
+                const uint32_t b_tap = b_lo0 + static_cast<uint32_t>((((p.r - 1 - r) * p.s + s) * Cfg::kBTap) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk) {
-                        const uint32_t accum = (r | s | kk) != 0 ? 1u : 0u;
-                        const uint32_t ad = a_tap + static_cast<uint32_t>(kk * 2);  // +32 bytes along K
-                        const uint32_t bd = b_tap + static_cast<uint32_t>((kk * Cfg::kMmaK * kRowBytes) >> 4);
-                        if constexpr (ELEM == ELEM_I8)
-                            ptx::mma_i8_elect_lh(d, ad, a_hi, bd, b_hi, idesc, accum);
-                        else
-                            ptx::mma_f16_elect_lh(d, ad, a_hi, bd, b_hi, idesc, accum);
-                    }
+                for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk) {
+                    const uint32_t accum = (first && kk == 0) ? 0u : 1u;
+                    const uint32_t ad = a_tap + static_cast<uint32_t>(kk * 2);  // +32 bytes along K
+                    const uint32_t bd = b_tap + static_cast<uint32_t>((kk * Cfg::kMmaK * kRowBytes) >> 4);
+                    if constexpr (ELEM == ELEM_I8)
+                        ptx::mma_i8_elect_lh(d_tap, ad, a_hi, both ? bd - b_lo0 + b_lo2 : bd, both ? b_hi2 : b_hi,
+                                             both ? idesc2 : idesc, accum);
+                    else
+                        ptx::mma_f16_elect_lh(d_tap, ad, a_hi, both ? bd - b_lo0 + b_lo2 : bd, both ? b_hi2 : b_hi,
+                                              both ? idesc2 : idesc, accum);
                 }
+            };
+            if constexpr (HB == 1) {
+                for (int r = 0; r < p.r; ++r)
+                    for (int s = 0; s < p.s; ++s)
+                        tap_mmas(d, (r * p.dh) * p.qp + s * p.dw, r, s, false, (r | s) == 0);
+            } else {
+                // sub-block 1's tap <r',s> = sub-block 0's tap <r'+dr, s> (same tile shift):
+                // 1) sub-block 1 taps without a partner (r' >= R - dr), 2) sub-block 0 taps without a
+                // partner (r < dr) -- both initialise their accumulators here -- 3) shared N = 128 taps
+                const int dr = share_dr;
+                const int r1_lo = dr > 0 ? p.r - dr : 0;
+                for (int r = r1_lo; r < p.r; ++r)
+                    for (int s = 0; s < p.s; ++s)
+                        tap_mmas(d + BN, (p.tpr + r * p.dh) * p.qp + s * p.dw, r, s, false, r == r1_lo && s == 0);
+                const int r0_hi = dr > 0 ? dr : p.r;
+                for (int r = 0; r < r0_hi; ++r)
+                    for (int s = 0; s < p.s; ++s)
+                        tap_mmas(d, (r * p.dh) * p.qp + s * p.dw, r, s, false, (r | s) == 0);
+                for (int r = dr; dr > 0 && r < p.r; ++r)
+                    for (int s = 0; s < p.s; ++s) tap_mmas(d, (r * p.dh) * p.qp + s * p.dw, r, s, true, false);
             }
             ptx::mma_commit_elect(&empty[stage]);
             ptx::mma_commit_elect(&tfull[acc]);
@@ -200,14 +241,17 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         uint32_t acc_phase = 0;
         uint32_t chunk_ctr = 0;
         for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+            const int pt = static_cast<int>(tile % p.p_tiles);
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
 #pragma unroll 1
-            for (int j = 0; j < BN / kOC; ++j) {
-                if (j * kOC >= p.k) continue;  // uniform (the store warp skips it too)
+            for (int jj = 0; jj < HB * (BN / kOC); ++jj) {
+                const int hb = jj / (BN / kOC), j = jj - hb * (BN / kOC);
+                // uniform (the store warp skips the same chunks)
+                if (j * kOC >= p.k || (pt * HB + hb) * p.tpr >= p.p) continue;
                 uint32_t v[kOC];
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                       static_cast<uint32_t>(acc * BN + j * kOC);
+                                       static_cast<uint32_t>(acc * HB * BN + hb * BN + j * kOC);
 #pragma unroll
                 for (int hh = 0; hh < kOC / 32; ++hh)
                     ptx::tmem_ld_32x32b_x32(taddr + hh * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * hh));
@@ -233,12 +277,14 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         for (long long tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
             const int pt = static_cast<int>(tile % p.p_tiles);
             const int n = static_cast<int>(tile / p.p_tiles);
-            for (int j = 0; j < BN / kOC; ++j) {
-                if (j * kOC >= p.k) continue;
+            for (int jj = 0; jj < HB * (BN / kOC); ++jj) {
+                const int hb = jj / (BN / kOC), j = jj - hb * (BN / kOC);
+                const int row0 = (pt * HB + hb) * p.tpr;
+                if (j * kOC >= p.k || row0 >= p.p) continue;
                 const uint32_t b = chunk_ctr & 1;
                 ptx::named_bar_sync(1 + b, 160);  // FULL(b)
                 if (lane == 0) {
-                    ptx::tma_store_4d(&tmap_y, smem_out + b * Cfg::kOutTile, j * kOC, 0, pt * p.tpr, n);  // clipped at P
+                    ptx::tma_store_4d(&tmap_y, smem_out + b * Cfg::kOutTile, j * kOC, 0, row0, n);  // clipped at P
                     ptx::tma_store_commit();
                     ptx::tma_store_wait_read<1>();
                 }

@@ -38,6 +38,7 @@ constexpr int kDbgNoSplitK = 1 << 19;     // never split the tail wave's k-loops
 constexpr int kDbgNoAutoPair = 1 << 21;   // never pick CTA pairs automatically
 constexpr int kDbgNoRowPairs = 1 << 22;   // row-band kernel: no N = 128 MMAs over two output rows
 constexpr int kDbgNoStemSpec = 1 << 23;   // row-band kernel: no compile-time stem instantiation
+constexpr int kDbgNoHaloStack = 1 << 25;  // halo kernel: one sub-block per block (no shared N = 128 taps)
 
 // Split-K arrival counters: one per tail tile, tagged with a launch generation
 // so they never need clearing; each launch uses one of 256 slices (so up to
@@ -245,10 +246,10 @@ int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandPa
 
 constexpr int kNotApplicable = -1000;  // internal: layer does not qualify for a specialised path
 
-template <int ELEM, int OUT, int BN>
+template <int ELEM, int OUT, int BN, int HB = 1>
 int launch_halo(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const HaloParams &p, int smem,
                 int grid, cudaStream_t st) {
-    auto kern = conv_halo_kernel<ELEM, OUT, BN>;
+    auto kern = conv_halo_kernel<ELEM, OUT, BN, HB>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
@@ -290,14 +291,16 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
     p.qp = static_cast<int>(Q) + (S - 1) * p.dw;
     if (p.qp > 128 || p.qp > 256) return kNotApplicable;
     p.tpr = 128 / p.qp;
-    p.tr = p.tpr + (R - 1) * p.dh;
+    // two stacked sub-blocks per block (BN = 64, 16-bit): taps shared across them run as N = 128 MMAs
+    const int hb = (K == 64 && E == 2 && !(g_debug_flags & kDbgNoHaloStack)) ? 2 : 1;
+    p.tr = hb * p.tpr + (R - 1) * p.dh;
     if (p.tr > 256) return kNotApplicable;
-    p.p_tiles = static_cast<int>((P + p.tpr - 1) / p.tpr);
+    p.p_tiles = static_cast<int>((P + hb * p.tpr - 1) / (hb * p.tpr));
     p.n_tiles = 1;
     p.tiles = static_cast<long long>(p.n) * p.p_tiles;
     p.a_box_bytes = p.tr * p.qp * 128;
     // the last taps read up to 128 + (R-1)*dh*QP + (S-1)*dw rows (rows past the box feed only discarded accumulator rows)
-    const int rows_read = std::max(p.tr * p.qp, 128 + (R - 1) * p.dh * p.qp + (S - 1) * p.dw);
+    const int rows_read = std::max(p.tr * p.qp, (hb - 1) * p.tpr * p.qp + 128 + (R - 1) * p.dh * p.qp + (S - 1) * p.dw);
     p.a_stage_bytes = (rows_read * 128 + 1023) / 1024 * 1024;
     p.b_bytes = R * S * K * 128;
     const int kOutTiles = 2 * kBM * 128;
@@ -358,7 +361,9 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
     if (grid > p.tiles) grid = static_cast<int>(p.tiles);
 #define IMCONV_HALO(EL, OUTK)                                                             \
     switch (K) {                                                                          \
-        case 64: return launch_halo<EL, OUTK, 64>(ta, tb, ty, p, smem, grid, st);         \
+        case 64:                                                                          \
+            if (hb == 2) return launch_halo<EL, OUTK, 64, 2>(ta, tb, ty, p, smem, grid, st); \
+            return launch_halo<EL, OUTK, 64>(ta, tb, ty, p, smem, grid, st);              \
         case 128: return launch_halo<EL, OUTK, 128>(ta, tb, ty, p, smem, grid, st);       \
         default: return launch_halo<EL, OUTK, 256>(ta, tb, ty, p, smem, grid, st);        \
     }
