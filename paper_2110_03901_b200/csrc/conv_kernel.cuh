@@ -11,14 +11,19 @@
 // (s*dw, r*dh); out-of-image pixels are zero-filled by the hardware, which is
 // the reference's "virtual padding", lowering.py:59-64).
 //
-// Warp roles (256 threads, one CTA per SM, persistent over output blocks):
-//   warp 0      : TMA producer (one elected lane)       -- operand generation
-//   warp 1      : tcgen05.mma issuer (one elected lane) -- contraction into TMEM
-//   warp 2      : TMEM allocator
-//   warps 4..7  : epilogue, TMEM -> registers -> NHWC global stores
+// Warp roles (320 threads, one CTA per SM, persistent over output blocks):
+//   warps 0, 2  : A (activation) TMA producers, even / odd stages (one lane each)
+//   warps 3, 8  : B (filter) TMA producers, even / odd stages
+//   warp 1      : tcgen05.mma issuer (warp-uniform issue, one elected lane)
+//   warp 2      : also the TMEM allocator
+//   warps 4..7  : epilogue, TMEM -> registers -> swizzled smem staging tiles
+//   warp 9      : output store issuer (one TMA store per staged 128 x 128-byte tile)
 // Pipelines: STAGES-deep smem ring (full/empty mbarriers, TMA complete_tx and
-// tcgen05.commit), and a 2-deep TMEM accumulator ring (tfull/tempty) so the
-// epilogue of block i overlaps the main loop of block i+1.
+// tcgen05.commit), a 2-deep TMEM accumulator ring (tfull/tempty) so the
+// epilogue of block i overlaps the main loop of block i+1, and two staging
+// tiles between the epilogue and the store warp (named barriers).  CG = 2
+// runs the block on a CTA pair (cta_group::2); split-K tail units and the
+// B-stationary mode are described at their code below.
 //
 // k-subtile order inside a block follows blocksched.order_subtiles
 // (blocksched.py:83-99): REUSE_AWARE = channel chunk outer / tap inner (the
