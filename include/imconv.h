@@ -182,7 +182,8 @@ typedef struct imconv_traffic {
     int64_t compulsory_read_bytes; /* distinct A and B lines touched x 128 */
     int64_t tiles;                 /* output blocks */
     int32_t bn, mt, grid, k_subtiles;
-    int32_t kernel;                /* kernel imconv_conv2d_nhwc picks: 0 generic, 1 row-band, 2 halo
+    int32_t kernel;                /* kernel imconv_conv2d_nhwc picks: 0 generic, 1 row-band, 2 halo,
+                                      3 halo with a streamed filter
                                       (the replay always models the generic raster) */
 } imconv_traffic;
 IMCONV_API int imconv_predict_traffic(const imconv_conv_args *args, int64_t l2_bytes, int32_t sms,

@@ -20,6 +20,7 @@
 #include "aux_kernels.cuh"
 #include "conv_kernel.cuh"
 #include "conv_halo.cuh"
+#include "conv_halo_stream.cuh"
 #include "conv_rowband.cuh"
 #include "lru.h"
 
@@ -39,6 +40,7 @@ constexpr int kDbgNoAutoPair = 1 << 21;   // never pick CTA pairs automatically
 constexpr int kDbgNoRowPairs = 1 << 22;   // row-band kernel: no N = 128 MMAs over two output rows
 constexpr int kDbgNoStemSpec = 1 << 23;   // row-band kernel: no compile-time stem instantiation
 constexpr int kDbgNoHaloStack = 1 << 25;  // halo kernel: one sub-block per block (no shared N = 128 taps)
+constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep the generic kernel
 
 // Split-K arrival counters: one per tail tile, tagged with a launch generation
 // so they never need clearing; each launch uses one of 256 slices (so up to
@@ -379,6 +381,131 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
         default: return kNotApplicable;
     }
 #undef IMCONV_HALO
+}
+
+template <int ELEM, int OUT, int BN>
+int launch_halo_stream(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const HaloStreamParams &p,
+                       int smem, int grid, cudaStream_t st) {
+    auto kern = conv_halo_stream_kernel<ELEM, OUT, BN, 2>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    });
+    if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
+    cudaError_t le = launch_pdl(kern, grid, kThreadsGeneric, smem, st, 1, ta, tb, ty, p);
+    if (le != cudaSuccess) return static_cast<int>(le);
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+// Halo tiles with a streamed filter (conv_halo_stream.cuh): stride 1, 16-bit pixels of
+// several 128-byte chunks (C = 128, 192, ...), K in {64, 128} (one or two 128-byte column
+// atoms; two stacked sub-blocks per block).  Each input pixel crosses L2 -> SM once per
+// block and chunk instead of R*S times.  Returns kNotApplicable otherwise.
+int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st) {
+    const int E = elem_bytes(a->in_dtype);
+    if (E != 2 || a->stride_h != 1 || a->stride_w != 1) return kNotApplicable;
+    if (a->c * E <= 128 || (a->c * E) % 128 != 0) return kNotApplicable;
+    if (a->tile_n != 0 || a->order == IMCONV_ORDER_FILTER_MAJOR) return kNotApplicable;
+    if (a->flags & (IMCONV_FLAG_NO_HALO | IMCONV_FLAG_CHANNEL_LAST)) return kNotApplicable;
+    if (g_debug_flags & kDbgNoHaloStream) return kNotApplicable;
+    const int K = static_cast<int>(a->k), R = static_cast<int>(a->r), S = static_cast<int>(a->s);
+    if (R * S == 1 || !(K == 64 || K == 128)) return kNotApplicable;
+    constexpr int HB = 2;
+    HaloStreamParams p{};
+    p.n = static_cast<int>(a->n);
+    p.h = static_cast<int>(a->h);
+    p.w = static_cast<int>(a->w_);
+    p.c = static_cast<int>(a->c);
+    p.k = K;
+    p.r = R;
+    p.s = S;
+    p.ph = a->pad_h;
+    p.pw = a->pad_w;
+    p.dh = a->dil_h;
+    p.dw = a->dil_w;
+    p.p = static_cast<int>(P);
+    p.q = static_cast<int>(Q);
+    p.qp = static_cast<int>(Q) + (S - 1) * p.dw;
+    if (p.qp > 128) return kNotApplicable;
+    p.tpr = 128 / p.qp;
+    p.tr = HB * p.tpr + (R - 1) * p.dh;
+    if (p.tr > 256) return kNotApplicable;
+    p.p_tiles = static_cast<int>((P + HB * p.tpr - 1) / (HB * p.tpr));
+    p.tiles = static_cast<long long>(p.n) * p.p_tiles;
+    p.chunks = static_cast<int>(a->c * E / 128);
+    p.a_box_bytes = p.tr * p.qp * 128;
+    const int rows_read =
+        std::max(p.tr * p.qp, (HB - 1) * p.tpr * p.qp + 128 + (R - 1) * p.dh * p.qp + (S - 1) * p.dw);
+    p.a_slot_bytes = (rows_read * 128 + 1023) / 1024 * 1024;
+    const int b_stage = K * 128;
+    const int fixed = 2 * kBM * 128 + 1024 /*align*/ + 1024 /*barriers*/;
+    p.na = 2;
+    p.nb = std::min(8, (kMaxDynSmem - fixed - p.na * p.a_slot_bytes) / b_stage);
+    if (p.nb < 3) return kNotApplicable;
+    const int smem = fixed + p.na * p.a_slot_bytes + p.nb * b_stage;
+
+    CUtensorMap ta, tb, ty;
+    std::memset(&ta, 0, sizeof(ta));
+    std::memset(&tb, 0, sizeof(tb));
+    std::memset(&ty, 0, sizeof(ty));
+    const int64_t N = a->n, H = a->h, W = a->w_, C = a->c;
+    const int nc = 128 / E;
+    {
+        cuuint64_t gdim[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(N)};
+        cuuint64_t gstride[3] = {static_cast<cuuint64_t>(C * E), static_cast<cuuint64_t>(W * C * E),
+                                 static_cast<cuuint64_t>(H * W * C * E)};
+        cuuint32_t box[4] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(p.qp),
+                             static_cast<cuuint32_t>(p.tr), 1};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (g_encode_tiled(&ta, tmap_dtype(a->in_dtype), 4, const_cast<void *>(a->x), gdim, gstride, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    {
+        cuuint64_t gdim[3] = {static_cast<cuuint64_t>(nc), static_cast<cuuint64_t>(R * S * C),
+                              static_cast<cuuint64_t>(K / nc)};
+        cuuint64_t gstride[2] = {static_cast<cuuint64_t>(K * E), static_cast<cuuint64_t>(nc * E)};
+        cuuint32_t box[3] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(K / nc)};
+        cuuint32_t es[3] = {1, 1, 1};
+        if (g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 3, const_cast<void *>(a->w), gdim, gstride, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    const int eo = a->out_dtype == IMCONV_F32 ? 4 : 2;
+    {
+        CUtensorMapDataType dt = a->out_dtype == IMCONV_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : a->out_dtype == IMCONV_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        cuuint64_t gdim[4] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(Q), static_cast<cuuint64_t>(P),
+                              static_cast<cuuint64_t>(N)};
+        cuuint64_t gstride[3] = {static_cast<cuuint64_t>(K * eo), static_cast<cuuint64_t>(Q * K * eo),
+                                 static_cast<cuuint64_t>(P * Q * K * eo)};
+        cuuint32_t box[4] = {static_cast<cuuint32_t>(128 / eo), static_cast<cuuint32_t>(Q),
+                             static_cast<cuuint32_t>(p.tpr), 1};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (g_encode_tiled(&ty, dt, 4, a->y, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
+    int grid = a->num_ctas > 0 ? a->num_ctas : sms;
+    if (grid > p.tiles) grid = static_cast<int>(p.tiles);
+    const bool f32 = a->out_dtype == IMCONV_F32;
+#define IMCONV_HS(EL, OUTK)                                                                   \
+    return K == 64 ? launch_halo_stream<EL, OUTK, 64>(ta, tb, ty, p, smem, grid, st)          \
+                   : launch_halo_stream<EL, OUTK, 128>(ta, tb, ty, p, smem, grid, st);
+    if (a->in_dtype == IMCONV_BF16) {
+        if (f32) { IMCONV_HS(ELEM_BF16, OUT_F32) } else { IMCONV_HS(ELEM_BF16, OUT_BF16) }
+    } else {
+        if (f32) { IMCONV_HS(ELEM_F16, OUT_F32) } else { IMCONV_HS(ELEM_F16, OUT_F16) }
+    }
+#undef IMCONV_HS
 }
 
 // Row-band path for 16-byte pixels (bf16/fp16, C = 8).  Returns kNotApplicable
@@ -797,6 +924,10 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
                      !(a->flags & IMCONV_FLAG_NO_HALO) && (K == 64 || K == 128 || K == 256) &&
                      R * S * K * 128 <= 120 * 1024)
                       ? 2
+                  : (E == 2 && C * E > 128 && (C * E) % 128 == 0 && a->stride_h == 1 && a->stride_w == 1 &&
+                     R * S > 1 && (K == 64 || K == 128) && Q + (S - 1) * a->dil_w <= 128 &&
+                     !(a->flags & IMCONV_FLAG_NO_HALO))
+                      ? 3
                       : 0;
     const int64_t x_lines = (N * H * W * C * E + 127) / 128;
     const int64_t w_lines = (R * S * C * K * E + 127) / 128;
@@ -984,6 +1115,8 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     if (!cl && !(a->flags & IMCONV_FLAG_NO_HALO)) {
         const int hr = try_halo(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
         if (hr != kNotApplicable) return hr;
+        const int hs = try_halo_stream(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
+        if (hs != kNotApplicable) return hs;
     }
 
     GenericPlan plan;

@@ -22,7 +22,7 @@ from . import _lib
 from .core import ConvSpec
 
 L2_BYTES_B200 = 126 * 1024 * 1024  # B200 L2 (both dies)
-KERNELS = {0: "generic", 1: "row-band", 2: "halo"}
+KERNELS = {0: "generic", 1: "row-band", 2: "halo", 3: "halo-stream"}
 
 
 @dataclass(frozen=True)

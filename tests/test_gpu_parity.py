@@ -566,3 +566,30 @@ def test_fp16_paths_exact(rng, case):
     assert np.array_equal(y.cpu().numpy(), want), case
     yh = P._kernels.conv2d_nhwc(xh, wh, *args)
     assert yh.dtype == torch.float16 and torch.equal(yh, y.half()), case
+
+
+@pytest.mark.parametrize("case", [
+    # (N, H, W, C, K, R, S, pad, dil): stride-1 layers with 16-bit pixels of several 128-byte
+    # chunks and K <= 128 -> halo tiles with a streamed filter
+    (2, 28, 28, 128, 128, 3, 3, 1, 1),   # ResNet s3 3x3
+    (3, 17, 13, 256, 64, 3, 3, 1, 1),    # ragged last block, K = 64
+    (2, 9, 11, 192, 128, 5, 3, 2, 1),    # 3 chunks, non-square filter
+    (2, 12, 12, 128, 128, 3, 3, 2, 2),   # dilation
+])
+def test_halo_stream_exact(rng, case):
+    """Streamed-filter halo kernel: exact against the oracle, equal to the generic kernel, and
+    its bf16 output is the fp32 result rounded once."""
+    P = _P()
+    from oracle import oracle as O
+    n, h, w_, c, k, r, s, pad, dil = case
+    args = (1, 1, pad, (s // 2) * dil, dil, dil)
+    x = rng.integers(-2, 3, size=(n, h, w_, c)).astype(np.int8)
+    w = rng.integers(-2, 3, size=(r, s, c, k)).astype(np.int8)
+    want = O.conv2d_nhwc_exact_f64(x, w, *args).astype(np.float32)
+    xb = torch.from_numpy(x).cuda().float().bfloat16()
+    wb = torch.from_numpy(w).cuda().float().bfloat16()
+    y = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32)
+    assert np.array_equal(y.cpu().numpy(), want), case
+    y_generic = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32, flags=P._lib.FLAG_NO_HALO)
+    assert torch.equal(y, y_generic)
+    assert torch.equal(P._kernels.conv2d_nhwc(xb, wb, *args), y.bfloat16())
