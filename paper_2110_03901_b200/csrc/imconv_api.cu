@@ -41,6 +41,7 @@ constexpr int kDbgNoRowPairs = 1 << 22;   // row-band kernel: no N = 128 MMAs ov
 constexpr int kDbgNoStemSpec = 1 << 23;   // row-band kernel: no compile-time stem instantiation
 constexpr int kDbgNoHaloStack = 1 << 25;  // halo kernel: one sub-block per block (no shared N = 128 taps)
 constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep the generic kernel
+constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-stationary layout
 
 // Split-K arrival counters: one per tail tile, tagged with a launch generation
 // so they never need clearing; each launch uses one of 256 slices (so up to
@@ -858,11 +859,27 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
 // stage + split-K partial round trip).  Measured (tools/small_n_probe.py,
 // N = 32): s4 1x1a 9.7 -> 8.0 us, s5 1x1a 14.5 -> 12.1, s4 3x3 16.3 -> 13.2;
 // s5 3x3 keeps 128 x 256 with a 5-way split (18.0 vs 19.4).
+inline bool R_S_is_1x1(const imconv_conv_args *a) { return a->r == 1 && a->s == 1; }
+
 int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, GenericPlan *g) {
     int rc = plan_generic_bn(a, P, Q, sms, a->tile_n, -1, g);
     if (rc || a->tile_n != 0 || g->bn != 256 || g->use_pair || (a->flags & (IMCONV_FLAG_CHANNEL_LAST |
                                                                              IMCONV_FLAG_KSUB1 | IMCONV_FLAG_MT1)))
         return rc;
+    if (R_S_is_1x1(a) && g->b_resident && g->tiles >= 8LL * sms && !(g_debug_flags & kDbgNo1x1Stream)) {
+        // Output-heavy 1x1 layers with a 1-2 k-subtile filter slice and many blocks: the streamed
+        // filter beats the B-stationary layout (measured, N >= 128: s2 1x1b / projection
+        // 90.5 -> 85.4 us with 128 x 128 blocks; s3 1x1b 47.2 -> 45.0 us with 128 x 256 blocks).
+        GenericPlan h;
+        if (g->k_subs == 1 && a->k >= 256 && plan_generic_bn(a, P, Q, sms, 128, 1, &h) == 0 && !h.use_pair) {
+            *g = h;
+            return 0;
+        }
+        if (g->k_subs == 2 && g->bn == 256 && plan_generic_bn(a, P, Q, sms, 256, 1, &h) == 0 && !h.use_pair) {
+            *g = h;
+            return 0;
+        }
+    }
     if (g->tiles >= sms) {
         // At least one wave of 128 x 256 blocks with the filter streamed (not B-stationary,
         // no split-K tail): CTA pairs (cta_group::2, 256 x 256 per pair, each CTA loads
