@@ -866,9 +866,9 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
     if (rc || a->tile_n != 0 || g->bn != 256 || g->use_pair || (a->flags & (IMCONV_FLAG_CHANNEL_LAST |
                                                                              IMCONV_FLAG_KSUB1 | IMCONV_FLAG_MT1)))
         return rc;
-    if (R_S_is_1x1(a) && g->b_resident && g->tiles >= 8LL * sms && !(g_debug_flags & kDbgNo1x1Stream)) {
-        // Output-heavy 1x1 layers with a 1-2 k-subtile filter slice and many blocks: the streamed
-        // filter beats the B-stationary layout (measured, N >= 128: s2 1x1b / projection
+    if (R_S_is_1x1(a) && g->b_resident && g->tiles >= 16LL * sms && !(g_debug_flags & kDbgNo1x1Stream)) {
+        // Output-heavy 1x1 layers with a 1-2 k-subtile filter slice and many blocks (>= 16 waves):
+        // the streamed filter beats the B-stationary layout (measured: s2 1x1b / projection
         // 90.5 -> 85.4 us with 128 x 128 blocks; s3 1x1b 47.2 -> 45.0 us with 128 x 256 blocks).
         GenericPlan h;
         if (g->k_subs == 1 && a->k >= 256 && plan_generic_bn(a, P, Q, sms, 128, 1, &h) == 0 && !h.use_pair) {
