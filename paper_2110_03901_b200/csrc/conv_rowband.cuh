@@ -64,7 +64,7 @@ struct RowbandParams {
     int dbg_flags;            // instrumentation: 1 = epilogue skips TMEM/stores, 2 = producer skips copies,
                               // 4 = one MMA per (row, filter row) instead of npairs, 8 = issuer skips MMAs,
                               // 16 = producer skips the proxy fence, 32 = one full-barrier arrive per warp,
-                              // 64 / 128 = epilogue / producer waits back off with nanosleep
+                              // 64 / 128 = epilogue / producer waits back off with nanosleep, 1 << 28 = no output stores
 };
 
 // instrumentation: cycles spent in a blocking wait, accumulated per role
@@ -521,7 +521,8 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                     const uint32_t b = chunk_ctr & 1;
                     ptx::named_bar_sync(1 + b, 160);  // FULL(b)
                     if (lane == 0) {
-                        ptx::tma_store_4d(&tmap_y, smem_out + b * Cfg::kOutTile, c * kOC, qb * 128, prow, n);
+                        if (!(IMCONV_INSTRUMENT && (p.dbg_flags & (1 << 28))))  // instrumentation: skip the output stores
+                            ptx::tma_store_4d(&tmap_y, smem_out + b * Cfg::kOutTile, c * kOC, qb * 128, prow, n);
                         ptx::tma_store_commit();
                         ptx::tma_store_wait_read<1>();
                     }
