@@ -62,6 +62,29 @@ def test_plan_matches_launcher_geometry():
     assert stem.kernel == "row-band"
 
 
+def test_planner_choices_on_resnet50():
+    """The planner's kernel / block-shape decisions for the ResNet-50 layers, as
+    reported by the host-side replay: a regression guard for the measured choices."""
+    from paper_2110_03901_b200.workloads import resnet50_layers
+    layers = {l.name: l.spec for l in resnet50_layers(256)}
+    expect = {
+        "stem": ("row-band", None),
+        "s2b1_3x3": ("halo", None),          # C = 64, stride 1: stacked halo sub-blocks
+        "s3b1_3x3": ("halo-stream", None),   # C = 128, stride 1, K = 128: streamed-filter halo tiles
+        "s3b0_3x3": ("generic", 128),        # stride 2
+        "s4b1_1x1b": ("generic", 256),       # B-stationary output layer
+        "s2b1_1x1b": ("generic", 128),       # output-heavy 1x1, >= 16 waves: streamed filter, 128-wide
+        "s4b1_3x3": ("generic", 256),
+    }
+    for name, (kernel, bn) in expect.items():
+        t = predict(layers[name])
+        assert t.kernel == kernel, name
+        if bn is not None:
+            assert t.bn == bn, name
+    # 32 images per GPU (8-GPU shard): stage-4 3x3 runs 128-wide blocks (more blocks than 256-wide)
+    assert predict(resnet50_layers(32)[[l.name for l in resnet50_layers(32)].index("s4b1_3x3")].spec).bn == 128
+
+
 def test_invalid_arguments():
     a = _lib.ImconvArgs()
     t = _lib.ImconvTraffic()
