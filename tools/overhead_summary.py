@@ -31,7 +31,7 @@ def ncu_segments(path):
         if "imconv::" not in key[1]:      # torch kernels creating the next layer's operands
             continue
         cur.append(by[key])
-        if "conv_fwd" in key[1] or "rowband" in key[1]:
+        if "imconv::conv_" in key[1]:  # any conv kernel (generic / row-band / halo) ends a segment
             segs.append(cur)
             cur = []
     tot = lambda seg, m: sum(k.get(m, 0.0) for k in seg)
