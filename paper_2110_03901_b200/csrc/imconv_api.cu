@@ -405,6 +405,17 @@ int launch_halo_stream(const CUtensorMap &ta, const CUtensorMap &tb, const CUten
 // several 128-byte chunks (C = 128, 192, ...), K in {64, 128} (one or two 128-byte column
 // atoms; two stacked sub-blocks per block).  Each input pixel crosses L2 -> SM once per
 // block and chunk instead of R*S times.  Returns kNotApplicable otherwise.
+// Wave quantisation against the generic kernel's 256-pixel blocks (K <= 128: one
+// column block): a halo-stream wave costs ~0.81 of a generic wave (s3 3x3, N = 128 / 256:
+// 7.2 vs 8.9 us per wave), so it is taken while ceil(halo tiles / SMs) <= 1.23 x
+// ceil(generic tiles / SMs).  Measured (tools/shape_sweep.py): N = 128 halo 4 waves
+// 29.5 us vs generic 3 waves 26.6 us; N = 256 halo 7 waves 50.0 vs generic 6 waves 52.6.
+inline bool halo_stream_wave_ok(long long halo_tiles, int64_t M, int sms) {
+    const long long gen_tiles = (M + 2 * kBM - 1) / (2 * kBM);
+    const long long wh = (halo_tiles + sms - 1) / sms, wg = (gen_tiles + sms - 1) / sms;
+    return 100 * wh <= 123 * wg;
+}
+
 int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st) {
     const int E = elem_bytes(a->in_dtype);
     if (E != 2 || a->stride_h != 1 || a->stride_w != 1) return kNotApplicable;
@@ -436,6 +447,7 @@ int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cu
     if (p.tr > 256) return kNotApplicable;
     p.p_tiles = static_cast<int>((P + HB * p.tpr - 1) / (HB * p.tpr));
     p.tiles = static_cast<long long>(p.n) * p.p_tiles;
+    if (a->num_ctas <= 0 && !halo_stream_wave_ok(p.tiles, a->n * P * Q, sms)) return kNotApplicable;
     p.chunks = static_cast<int>(a->c * E / 128);
     p.a_box_bytes = p.tr * p.qp * 128;
     const int rows_read =
@@ -828,13 +840,16 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
         // Measured (tools/small_n_probe.py): the partials' L2 round trip (write 4 B per
         // output, fence, peer wait, bulk read back) costs ~5-7k cycles per split, so only
         // long k-loops gain (3x3 with C >= 256: 36+ stages); 16-32-stage 1x1 layers lose.
-        constexpr int kSkMaxSplit = 5, kSkMinStages = 36;
+        constexpr int kSkMaxSplit = 5, kSkMinStages = 36, kSkCyclesPerSplit = 15000;
         const bool sub_wave = g->tiles < g0 && k_st >= kSkMinStages;
         const bool short_tail = tail > 0 && 2 * tail <= g0 && g->tiles < 2 * g0 && k_st >= kSkMinStages;
         if (sub_wave || short_tail) {
             const int Sk = static_cast<int>(std::min<long long>(
                 {g0 / tail, static_cast<long long>(k_st / 4), kSkMaxSplit}));
-            if (Sk >= 2) {
+            // and only when the stages saved (k_st * (1 - 1/S) at ~600 cycles) beat the
+            // ~15k-cycle partial round trip: a 3-way split of a 36-stage tail loses
+            // (s4 3x3 at N = 128: 31.6 us split vs 29.3 us with CTA pairs)
+            if (Sk >= 2 && static_cast<long long>(k_st) * (Sk - 1) > static_cast<long long>(kSkCyclesPerSplit / 600) * Sk) {
                 g->sk_split = Sk;
                 g->sk_tail = tail;
                 if (g->tiles < g0) grid = static_cast<int>(tail * Sk);
@@ -895,16 +910,22 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
     }
     GenericPlan h;
     if (plan_generic_bn(a, P, Q, sms, 128, 1, &h) != 0 || h.use_pair) return 0;
+    // Full waves run k_st stages per block; a split-K tail runs k_st / S stages plus the
+    // partials' round trip.  Cycles per stage in this latency-bound regime, fitted to
+    // tools/shape_sweep.py at N = 32 / 128: ~600 for a 128 x 256 x 64 stage (48 KB of
+    // operands), ~900 for a 2-k-subtile 128 x 128 stage (64 KB, same tensor work);
+    // ~15k cycles per split-K tail (s5 3x3 at N = 128: 128 x 256 blocks 29.0 us vs
+    // 128 x 128 blocks + split tail 36.7 us; s4 3x3 at N = 32: 128 x 128 13.2 vs
+    // 128 x 256 + 3-way split 16.3).
     auto cost = [&](const GenericPlan &q, double cyc_stage) {
-        const long long k_st = (q.k_subs + q.ksub - 1) / q.ksub;
-        const long long units = q.sk_split > 1 ? (q.tiles - q.sk_tail) + q.sk_tail * q.sk_split : q.tiles;
-        const long long waves = (units + q.grid - 1) / q.grid;
-        const double per = static_cast<double>(k_st) / q.sk_split * cyc_stage + (q.sk_split > 1 ? 6000.0 : 0.0);
-        return static_cast<double>(waves) * per;
+        const double k_st = static_cast<double>((q.k_subs + q.ksub - 1) / q.ksub);
+        const long long full = q.tiles - q.sk_tail;
+        const long long full_waves = (full + q.grid - 1) / q.grid;
+        const long long tail_waves = q.sk_split > 1 ? (q.sk_tail * q.sk_split + q.grid - 1) / q.grid : 0;
+        return static_cast<double>(full_waves) * k_st * cyc_stage +
+               static_cast<double>(tail_waves) * (k_st / q.sk_split * cyc_stage + 15000.0);
     };
-    // cycles per pipeline stage in this latency-bound regime (measured ~600 for
-    // 128 x 256 x 64; a 2-k-subtile 128 x 128 stage carries the same tensor work)
-    if (cost(h, 600.0) < cost(*g, 600.0)) *g = h;
+    if (cost(h, 900.0) < cost(*g, 600.0)) *g = h;
     return 0;
 }
 
@@ -943,7 +964,10 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
                       ? 2
                   : (E == 2 && C * E > 128 && (C * E) % 128 == 0 && a->stride_h == 1 && a->stride_w == 1 &&
                      R * S > 1 && (K == 64 || K == 128) && Q + (S - 1) * a->dil_w <= 128 &&
-                     !(a->flags & IMCONV_FLAG_NO_HALO))
+                     !(a->flags & IMCONV_FLAG_NO_HALO) &&
+                     (a->num_ctas > 0 || halo_stream_wave_ok(N * ((P + 2 * (128 / (Q + (S - 1) * a->dil_w)) - 1) /
+                                                                 (2 * (128 / (Q + (S - 1) * a->dil_w)))),
+                                                            M, sms)))
                       ? 3
                       : 0;
     const int64_t x_lines = (N * H * W * C * E + 127) / 128;

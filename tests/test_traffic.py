@@ -83,6 +83,15 @@ def test_planner_choices_on_resnet50():
             assert t.bn == bn, name
     # 32 images per GPU (8-GPU shard): stage-4 3x3 runs 128-wide blocks (more blocks than 256-wide)
     assert predict(resnet50_layers(32)[[l.name for l in resnet50_layers(32)].index("s4b1_3x3")].spec).bn == 128
+    # 128 images per GPU (2-GPU shard): s5 3x3 keeps 128 x 256 blocks (no split-K tail on 128 x 128),
+    # s4 3x3 runs CTA pairs (a 3-way split of a 36-stage tail loses), s3 3x3 the generic kernel
+    # (4 halo-stream waves vs 3 generic waves)
+    l128 = {l.name: l.spec for l in resnet50_layers(128)}
+    t = predict(l128["s5b1_3x3"])
+    assert (t.bn, t.tiles, t.grid) == (256, 98, 98)
+    t = predict(l128["s4b1_3x3"])
+    assert (t.bn, t.tiles) == (256, 98)  # 98 CTA-pair blocks of 256 x 256
+    assert predict(l128["s3b1_3x3"]).kernel == "generic"
 
 
 def test_invalid_arguments():
