@@ -63,6 +63,11 @@ extern "C" {
 #define IMCONV_FLAG_CHANNEL_LAST 64 /* channel-last BASELINE (bf16/fp16): reduction order
                                      k = (c, r, s), A gathered element by element -- the
                                      paper's CL lowering, for the stride contrast only        */
+#define IMCONV_FLAG_STATIC_FILTER 128 /* the caller guarantees the filter is not written by any
+                                     kernel still in flight on the stream (weights uploaded or
+                                     converted before the step): the kernel's filter loads then
+                                     start before its programmatic-launch wait, overlapping the
+                                     previous conv's tail.  Inputs are always ordered.         */
 
 /*
  * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,

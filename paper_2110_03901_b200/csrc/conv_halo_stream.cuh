@@ -26,6 +26,7 @@
 namespace imconv {
 
 struct HaloStreamParams {
+    int b_early;  // 1: static filter -- the B producer (warp 3) starts before griddepcontrol.wait
     int n, h, w, c, k;
     int r, s, ph, pw, dh, dw;
     int p, q;
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     const uint32_t tmem_base = *tmem_slot;
     // PDL: setup above overlaps the previous kernel's tail
     ptx::griddep_launch_dependents();
-    ptx::griddep_wait();
+    if (!(p.b_early && warp == 3)) ptx::griddep_wait();
 
     if (warp == 0) {
         if (lane == 0) {

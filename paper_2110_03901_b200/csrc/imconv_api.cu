@@ -279,6 +279,7 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
     if (R * S == 1) return kNotApplicable;
     if (K % nc != 0 || !(K == 64 || K == 128 || K == 256) || (E == 1 && K < 128)) return kNotApplicable;
     HaloParams p{};
+    p.b_early = (a->flags & IMCONV_FLAG_STATIC_FILTER) ? 1 : 0;
     p.n = static_cast<int>(a->n);
     p.h = static_cast<int>(a->h);
     p.w = static_cast<int>(a->w_);
@@ -427,6 +428,7 @@ int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cu
     if (R * S == 1 || !(K == 64 || K == 128)) return kNotApplicable;
     constexpr int HB = 2;
     HaloStreamParams p{};
+    p.b_early = (a->flags & IMCONV_FLAG_STATIC_FILTER) ? 1 : 0;
     p.n = static_cast<int>(a->n);
     p.h = static_cast<int>(a->h);
     p.w = static_cast<int>(a->w_);
@@ -530,6 +532,7 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     const int BN = K <= 64 ? 64 : (K <= 128 ? 128 : 256);
     const int TP = 256 / BN;
     RowbandParams p{};
+    p.b_early = (a->flags & IMCONV_FLAG_STATIC_FILTER) ? 1 : 0;
     p.n = static_cast<int>(a->n);
     p.h = static_cast<int>(a->h);
     p.w = static_cast<int>(a->w_);
@@ -1322,6 +1325,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         p.k_stages = plan.k_subs;
     }
     p.dbg_flags = g_debug_flags & 0xff;
+    p.b_early = (!cl && (a->flags & IMCONV_FLAG_STATIC_FILTER)) ? 1 : 0;
 
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = plan.grid;

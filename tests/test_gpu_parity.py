@@ -593,3 +593,46 @@ def test_halo_stream_exact(rng, case):
     y_generic = P._kernels.conv2d_nhwc(xb, wb, *args, out_dtype=torch.float32, flags=P._lib.FLAG_NO_HALO)
     assert torch.equal(y, y_generic)
     assert torch.equal(P._kernels.conv2d_nhwc(xb, wb, *args), y.bfloat16())
+
+
+def test_static_filter_dependent_chain():
+    """IMCONV_FLAG_STATIC_FILTER: the filter loads start before the programmatic-launch wait.
+    A chain of dependent convs through every kernel family (row-band stem, stacked halo, generic
+    1x1, streamed-filter halo, generic strided 3x3), queued back to back into NaN-filled output
+    buffers, must give each layer exactly what a separate flag-free launch on the same input gives:
+    an input read before the previous grid finished would show up as NaN or stale values."""
+    P = _P()
+    from paper_2110_03901_b200._kernels import conv_device
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(7)
+    # (C, K, R, stride, pad): input 64x64 with C = 8 (stem-like, 3 live channels)
+    chain = [(8, 64, 7, 2, 3), (64, 64, 3, 1, 1), (64, 128, 1, 1, 0), (128, 128, 3, 1, 1), (128, 256, 3, 2, 1)]
+    x0 = torch.randn((4, 64, 64, 8), device=dev, generator=g)
+    x0[..., 3:] = 0
+    x0 = x0.bfloat16()
+    ws, ys, args = [], [], []
+    h = 64
+    for c, k, r, st, pad in chain:
+        w = (torch.randn((r, r, c, k), device=dev, generator=g) * (2.0 / (r * r * c)) ** 0.5).bfloat16()
+        ho = (h + 2 * pad - r) // st + 1
+        ws.append(w)
+        ys.append(torch.full((4, ho, ho, k), float("nan"), device=dev, dtype=torch.bfloat16))
+        args.append((st, st, pad, pad, 1, 1))
+        h = ho
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for y in ys:
+            y.fill_(float("nan"))
+        torch.cuda.synchronize()
+        inp = x0
+        for w, y, a in zip(ws, ys, args):
+            conv_device(inp, w, *a, y=y, flags=P._lib.FLAG_STATIC_FILTER)
+            inp = y
+        torch.cuda.synchronize()
+        inp = x0
+        for i, (w, y, a) in enumerate(zip(ws, ys, args)):
+            ref = conv_device(inp, w, *a)
+            torch.cuda.synchronize()
+            assert not torch.isnan(y).any(), (rep, i)
+            assert torch.equal(y, ref), (rep, i)
+            inp = y
