@@ -1,6 +1,6 @@
 """Seeded random mid-size convolutions aimed at every kernel path (row-band, halo with stacked
 sub-blocks, generic single / CTA pairs / split-K / B-stationary), integer-valued bf16 with fp32
-output and int8: bit-exact against the oracle."""
+output and int8: bit-exact against the oracle (bf16 also with IMCONV_FLAG_STATIC_FILTER)."""
 
 import numpy as np
 import pytest
@@ -55,6 +55,9 @@ def test_random_mid_size_exact(seed):
         fb = torch.from_numpy(f).cuda().float().bfloat16()
         y = P._kernels.conv2d_nhwc(xb, fb, *args, out_dtype=torch.float32)
         assert np.array_equal(y.cpu().numpy(), want.astype(np.float32)), case
+        # filter loads ahead of the programmatic-launch wait: same bits on every path
+        ys = P._kernels.conv2d_nhwc(xb, fb, *args, out_dtype=torch.float32, flags=P._lib.FLAG_STATIC_FILTER)
+        assert torch.equal(ys, y), case
         if (c % 16 == 0) and (k % 16 == 0):
             yi = P._kernels.conv2d_nhwc(torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda(), *args)
             assert np.array_equal(yi.cpu().numpy(), want), case
