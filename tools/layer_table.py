@@ -2,7 +2,9 @@
 """Per-layer table from an ncu launch list of one bench step (53 launches, in
 resnet50_layers order): device time, DRAM bytes, roofline fraction.
 
-  python tools/layer_table.py gpurun_out/launches.csv [--group]
+  python tools/layer_table.py gpurun_out/launches.csv [--group] [--n 32]
+
+--n: the per-GPU batch the launch list was taken at (an emulated shard), default 256.
 """
 import csv
 import sys
@@ -12,10 +14,10 @@ sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(_
 from paper_2110_03901_b200.lowering import touched_pixels  # noqa: E402
 from paper_2110_03901_b200.workloads import resnet50_layers  # noqa: E402
 
-PEAK_TF, HBM = 1395.7, 6540.2  # MEASURED_PEAKS.json (bf16 sustained, copy GB/s)
+PEAK_TF, HBM = 1412.1, 6550.4  # MEASURED_PEAKS.json (bf16 sustained, copy GB/s)
 
 
-def main(path, group):
+def main(path, group, n=256):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
     iid, im, iv = h.index("ID"), h.index("Metric Name"), h.index("Metric Value")
@@ -26,7 +28,7 @@ def main(path, group):
             per[r[iid]] = {}
             order.append(r[iid])
         per[r[iid]][r[im]] = float(r[iv].replace(",", ""))
-    layers = resnet50_layers(256)
+    layers = resnet50_layers(n)
     assert len(order) == len(layers), (len(order), len(layers))
     agg = {}
     tot_t = tot_roof = tot_traffic = tot_alg = 0.0
@@ -62,4 +64,6 @@ def main(path, group):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], "--group" in sys.argv)
+    argv = sys.argv[1:]
+    n = int(argv[argv.index("--n") + 1]) if "--n" in argv else 256
+    main(argv[0], "--group" in argv, n)
