@@ -411,6 +411,13 @@ int launch_halo_stream(const CUtensorMap &ta, const CUtensorMap &tb, const CUten
 // 7.2 vs 8.9 us per wave), so it is taken while ceil(halo tiles / SMs) <= 1.23 x
 // ceil(generic tiles / SMs).  Measured (tools/shape_sweep.py): N = 128 halo 4 waves
 // 29.5 us vs generic 3 waves 26.6 us; N = 256 halo 7 waves 50.0 vs generic 6 waves 52.6.
+// blocks of the halo-stream kernel: per image, output-row groups of two sub-blocks of
+// tpr = 128 / QP rows each (QP = Q + (S-1)*dw, the padded pitch)
+inline long long halo_stream_tiles(int64_t N, int64_t P, int64_t Q, int64_t S, int dw) {
+    const int64_t rows = 2 * (128 / (Q + (S - 1) * dw));
+    return N * ((P + rows - 1) / rows);
+}
+
 inline bool halo_stream_wave_ok(long long halo_tiles, int64_t M, int sms) {
     const long long gen_tiles = (M + 2 * kBM - 1) / (2 * kBM);
     const long long wh = (halo_tiles + sms - 1) / sms, wg = (gen_tiles + sms - 1) / sms;
@@ -757,6 +764,9 @@ struct GenericPlan {
 
 // One candidate block shape: bn output channels, variant_force >= 0 overrides
 // the m-tile / k-subtile variant (see dispatch_bn).
+// split-K: cycles one split tail pays for the partials' L2 round trip (fitted, see plan_generic)
+constexpr int kSkCyclesPerSplit = 15000;
+
 int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, int bn_req, int variant_force,
                     GenericPlan *g, bool pair_force = false) {
     const int64_t K = a->k, R = a->r, S = a->s, C = a->c;
@@ -843,7 +853,7 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
         // Measured (tools/small_n_probe.py): the partials' L2 round trip (write 4 B per
         // output, fence, peer wait, bulk read back) costs ~5-7k cycles per split, so only
         // long k-loops gain (3x3 with C >= 256: 36+ stages); 16-32-stage 1x1 layers lose.
-        constexpr int kSkMaxSplit = 5, kSkMinStages = 36, kSkCyclesPerSplit = 15000;
+        constexpr int kSkMaxSplit = 5, kSkMinStages = 36;
         const bool sub_wave = g->tiles < g0 && k_st >= kSkMinStages;
         const bool short_tail = tail > 0 && 2 * tail <= g0 && g->tiles < 2 * g0 && k_st >= kSkMinStages;
         if (sub_wave || short_tail) {
@@ -926,7 +936,7 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
         const long long full_waves = (full + q.grid - 1) / q.grid;
         const long long tail_waves = q.sk_split > 1 ? (q.sk_tail * q.sk_split + q.grid - 1) / q.grid : 0;
         return static_cast<double>(full_waves) * k_st * cyc_stage +
-               static_cast<double>(tail_waves) * (k_st / q.sk_split * cyc_stage + 15000.0);
+               static_cast<double>(tail_waves) * (k_st / q.sk_split * cyc_stage + kSkCyclesPerSplit);
     };
     if (cost(h, 900.0) < cost(*g, 600.0)) *g = h;
     return 0;
@@ -968,9 +978,7 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
                   : (E == 2 && C * E > 128 && (C * E) % 128 == 0 && a->stride_h == 1 && a->stride_w == 1 &&
                      R * S > 1 && (K == 64 || K == 128) && Q + (S - 1) * a->dil_w <= 128 &&
                      !(a->flags & IMCONV_FLAG_NO_HALO) &&
-                     (a->num_ctas > 0 || halo_stream_wave_ok(N * ((P + 2 * (128 / (Q + (S - 1) * a->dil_w)) - 1) /
-                                                                 (2 * (128 / (Q + (S - 1) * a->dil_w)))),
-                                                            M, sms)))
+                     (a->num_ctas > 0 || halo_stream_wave_ok(halo_stream_tiles(N, P, Q, S, a->dil_w), M, sms)))
                       ? 3
                       : 0;
     const int64_t x_lines = (N * H * W * C * E + 127) / 128;
