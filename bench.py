@@ -3,10 +3,15 @@
 
 Default workload (BASELINE.json configs[3], "cfg4"): one step = the 53
 convolution layers of ResNet-50 v1.5 at 224x224, batch 256 sharded evenly
-over the ranks (strong scaling: the global batch is fixed, each GPU takes 256/N images), bf16 in / bf16 out, fp32
-accumulation, synthetic N(0,1) activations and Kaiming weights.
+over the ranks (strong scaling: the global batch is fixed, each GPU takes 256/N
+images), bf16 in / bf16 out, fp32 accumulation, synthetic N(0,1) activations
+and Kaiming weights.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
+
+``--gpus N`` (N > 1) without a torchrun environment re-launches this script
+under ``torch.distributed.run`` with N ranks, one GPU each (NCCL); under
+torchrun the ranks read RANK / LOCAL_RANK / WORLD_SIZE.
 
 Prints ONE JSON line on rank 0 (contract in the task statement):
   value       = whole-job conv TFLOP/s, inputs resident in HBM, device-timed
@@ -14,18 +19,27 @@ Prints ONE JSON line on rank 0 (contract in the task statement):
   e2e         = the same metric through the public API with pinned HOST
                 buffers: H2D of every layer's input+filter, the kernel, D2H of
                 every output, inside the timed region;
-  roofline    = the conv kernel against the measured bf16 peak;
-  cpu_baseline= the CPU oracle port (oracle/, numpy+OpenBLAS taps -- the
-                reference's own float algorithm, _fallback.py:17-42) on a
-                bounded sample of the same workload, rank 0 only.
---impl reference runs only that CPU implementation (rank 0; others exit 0).
+  roofline    = the conv kernels against the measured bf16 peak (burst peak for
+                a timed region under 1 s, sustained above);
+  parity      = after the timed region every layer's output shards are
+                all-gathered (NCCL) and the first and last image of every
+                rank's shard are checked against the CPU oracle;
+  cpu_baseline= the reference's own CPU kernels compiled from its sources
+                (oracle/_ref: _fallback.conv2d_nhwc, _fallback.py:17-42, for
+                floats; _native.conv2d_nhwc, _native.pyx:20-47, for ints), else
+                the oracle port, on a bounded sample of the same workload,
+                rank 0 only.
+--impl reference runs only that CPU implementation (rank 0; others exit 0) on
+the same workload and prints the same `config`.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,33 +51,41 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 METRIC = "conv TFLOP/s (2*N*K*C*R*S*P*Q/time)"
+L2_BYTES = 126 * 1024 * 1024       # B200 L2 (both dies): the rotation decision must not depend on the arm
+BURST_REGION_MS = 1000.0           # timed regions shorter than this are compared with the burst peak
+PARITY_TOL = 1e-2                  # north_star: normalised max error of bf16 output vs the fp32 oracle
 
 
-def committed_traffic(config: str):
-    """DRAM bytes per step from the newest committed ncu launch list of this
-    workload (profiles/r*/launches_*.csv: dram__bytes_read + write summed over
-    the step's launches), or None."""
-    import csv
-    import glob
-    if config != "cfg4":
-        return None, None
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "launches_*.csv")))  # newest round / letter last
-    for path in reversed(files):
-        try:
-            rows = [r for r in csv.reader(open(path)) if len(r) > 10]
-            h = rows[0]
-            im, iv, iid = h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
-            ids = set()
-            tot = 0.0
-            for r in rows[1:]:
-                ids.add(r[iid])
-                if r[im] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                    tot += float(r[iv].replace(",", ""))
-            if len(ids) == 53 and tot > 0:
-                return tot, os.path.relpath(path, ROOT)
-        except Exception:
-            continue
-    return None, None
+# ------------------------------------------------------------------ helpers
+
+def csrc_fingerprint() -> str:
+    """sha256 over the kernel sources and the C ABI header: committed ncu traffic is
+    reported only for the build it was captured from."""
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2110_03901_b200", "csrc")
+    for name in sorted(os.listdir(csrc)):
+        if name.endswith((".cu", ".cuh", ".h", ".cpp")):
+            h.update(name.encode())
+            with open(os.path.join(csrc, name), "rb") as fh:
+                h.update(fh.read())
+    with open(os.path.join(ROOT, "include", "imconv.h"), "rb") as fh:
+        h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def committed_traffic(config: str, world: int):
+    """DRAM bytes per step per GPU from the committed ncu summary of this workload
+    (profiles/traffic_<config>_w<world>.json, written by tools/traffic_summary.py from a
+    launch list with dram__bytes_read/write).  Returns (bytes or None, note)."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{config}_w{world}.json")
+    if not os.path.exists(path):
+        return None, f"no committed ncu traffic for {config} at {world} GPU(s)"
+    with open(path) as fh:
+        d = json.load(fh)
+    if d.get("csrc_sha") != csrc_fingerprint():
+        return None, f"committed ncu traffic ({d.get('source')}) is from another build of the kernels: not reported"
+    return float(d["dram_bytes_per_step"]), (f"committed ncu launch list {d.get('source')} of this build "
+                                             f"(csrc {d['csrc_sha']}; not measured in this run)")
 
 
 def load_peaks():
@@ -75,8 +97,6 @@ def load_peaks():
     except Exception:
         return dict(PEAKS_FALLBACK), "fallback"
 
-
-# ------------------------------------------------------------------ helpers
 
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
@@ -134,6 +154,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int, argv) -> int:
+    """`--gpus N` outside torchrun: re-launch this script with N ranks (one GPU each).
+    Rank 0's stdout carries the JSON line; the exit code is the launcher's."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
 def dist_setup():
     import torch
     import torch.distributed as dist
@@ -141,7 +177,11 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -163,82 +203,219 @@ def cpu_threads():
     return os.cpu_count() or 1
 
 
-# ------------------------------------------------------------------ CPU arm
-
-def cpu_reference_step(layers, n_sample: int, seed: int = 1):
-    """The reference's CPU algorithm (oracle port: per-tap strided slice @
-    w[r,s] through OpenBLAS, _fallback.py:17-42; int8 layers through the int64
-    loop, _native.pyx:20-47) over every layer at batch n_sample.  Returns
-    (seconds, flops)."""
-    import numpy as np
-    from oracle import oracle as O
-    from paper_2110_03901_b200.workloads import synthetic_operands
-
-    secs, flops = 0.0, 0
-    for layer in layers:
-        sp = layer.spec.with_batch(n_sample)
-        x, w = synthetic_operands(layer, seed=seed, n=n_sample)
-        if layer.dtype == "int8":
-            xn, wn = x.numpy(), w.numpy()
-            t0 = time.perf_counter()
-            O.conv2d_nhwc_i64(xn, wn, *sp.conv_args(), threads=cpu_threads())
-        else:
-            xn, wn = x.float().numpy(), w.float().numpy()
-            t0 = time.perf_counter()
-            O.conv2d_nhwc_taps(xn, wn, *sp.conv_args())
-        secs += time.perf_counter() - t0
-        flops += sp.flops
-        del x, w
-    return secs, flops
-
-
-def run_reference_arm(args, layers, world, rank):
-    if rank != 0:
-        return 0
-    # torchrun exports OMP_NUM_THREADS=1 to every rank; the reference arm is rank 0 alone,
-    # so it takes all host threads for OpenBLAS
+def use_all_host_threads():
+    # torchrun exports OMP_NUM_THREADS=1 to every rank; the CPU legs run on rank 0 alone,
+    # so they take every host thread for OpenBLAS
     try:
         from threadpoolctl import threadpool_limits
         threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")
     except Exception:
         pass
-    n_sample = args.ref_sample
-    for _ in range(args.warmup):
-        cpu_reference_step(layers[:1], 1)
-    times, flops = [], 0
-    for _ in range(args.steps):
-        s, flops = cpu_reference_step(layers, n_sample)
-        times.append(s)
+
+
+def bytes_alg(sp, dtype: str, out_elem: int) -> int:
+    """e_in*N*T*C + e_in*R*S*C*K + e_out*N*P*Q*K (T = distinct input pixels touched)."""
+    from paper_2110_03901_b200.lowering import touched_pixels
+    ei = 1 if dtype == "int8" else 2
+    return sp.n * touched_pixels(sp) * sp.c_i * ei + sp.h_f * sp.w_f * sp.c_i * sp.c_o * ei \
+        + sp.gemm_m * sp.c_o * out_elem
+
+
+def rotation_copies(layers, world: int) -> int:
+    """Copies of the working set a step rotates over so that no timed pass reads L2-resident
+    inputs (1 when one pass already streams more than twice the L2)."""
+    b = 0
+    for li, layer in enumerate(layers):
+        lo, hi = shard_batch(layer.spec.n, world, 0)
+        b += bytes_alg(layer.spec.with_batch(hi - lo), layer.dtype, 4 if layer.dtype == "int8" else 2)
+    return 1 if b >= 2 * L2_BYTES else -(-2 * L2_BYTES // max(b, 1))
+
+
+def workload_config(name: str, layers, world: int) -> dict:
+    """The `config` object both arms print (identical, so the driver compares like with like)."""
+    lo, hi = shard_batch(layers[0].spec.n, world, 0)
+    copies = rotation_copies(layers, world)
+    per_gpu = 0
+    for layer in layers:
+        l0, h0 = shard_batch(layer.spec.n, world, 0)
+        per_gpu += bytes_alg(layer.spec.with_batch(h0 - l0), layer.dtype, 4 if layer.dtype == "int8" else 2)
+    l2 = (f"inputs larger than L2: every layer has its own buffers, per-step working set "
+          f"{per_gpu / 1e9:.1f} GB per GPU" if copies == 1 else
+          f"each timed pass reads L2-cold inputs: the captured step rotates over {copies} copies of the "
+          f"{per_gpu / 1e6:.1f} MB working set ({copies * per_gpu / 1e6:.0f} MB > 2 x L2)")
+    cfg = {"workload": name + (" (ResNet-50 v1.5, 53 convs, 224x224)" if name == "cfg4" else ""),
+           "global_batch": layers[0].spec.n, "per_gpu_batch": hi - lo, "layers": len(layers),
+           "parallelism": f"dp{world} (N-sharded, no collective)", "l2": l2}
+    return cfg
+
+
+def make_operands(layer, sp, li: int, lo: int, dev):
+    """Operands of one rank's shard (images [lo, lo + sp.n) of the global batch): seeded by
+    (layer, shard start) so any rank -- rank 0 when verifying -- can regenerate any shard;
+    weights seeded by the layer alone (replicated on every rank)."""
+    import torch
+    g = torch.Generator(device=dev).manual_seed(1000 + 7919 * li + lo)
+    gw = torch.Generator(device=dev).manual_seed(2000 + li)
+    xs = (sp.n, sp.h_i, sp.w_i, sp.c_i)
+    ws = (sp.h_f, sp.w_f, sp.c_i, sp.c_o)
+    if layer.dtype == "int8":
+        x = torch.randint(-128, 128, xs, generator=g, device=dev, dtype=torch.int16).to(torch.int8)
+        w = torch.randint(-128, 128, ws, generator=gw, device=dev, dtype=torch.int16).to(torch.int8)
+        return x, w
+    x = torch.randn(xs, generator=g, device=dev, dtype=torch.float32)
+    if layer.relu_input:
+        x.clamp_(min=0)
+    w = torch.randn(ws, generator=gw, device=dev, dtype=torch.float32) * (2.0 / (sp.c_i * sp.h_f * sp.w_f)) ** 0.5
+    if layer.name == "stem":
+        x[..., 3:] = 0
+        w[:, :, 3:, :] = 0
+    return x.to(torch.bfloat16), w.to(torch.bfloat16)
+
+
+# ------------------------------------------------------------------ CPU legs
+
+def cpu_impl():
+    """(conv function, kind, description): the reference's kernels compiled from its
+    sources (oracle/_ref) when present, else the oracle port."""
+    from oracle import ref as R
+    if R.available():
+        return R.conv2d_nhwc, "reference", ("the reference's own kernels compiled from its sources "
+                                            "(oracle/_ref: _fallback.conv2d_nhwc for floats, "
+                                            "_native.conv2d_nhwc for ints)")
+    from oracle import oracle as O
+    return O.conv_reference, "port", "oracle port of the reference's kernels (oracle/oracle.py)"
+
+
+def cpu_layer_operands(layer, sp, li: int):
+    """Host operands in the reference's dtypes: bf16-rounded floats as fp32 (the GPU arm
+    computes on the same bf16 values), ints as int64 (the reference's _norm)."""
+    import torch
+    x, w = make_operands(layer, sp, li, 0, torch.device("cpu"))
+    if layer.dtype == "int8":
+        return x.numpy().astype("int64"), w.numpy().astype("int64")
+    return x.float().numpy(), w.float().numpy()
+
+
+def cpu_time_layers(layers, n_sample, conv, reps: int = 1, budget_s: float | None = None):
+    """Time `conv` over every layer at batch n_sample (or the full batch when None), `reps`
+    passes, layer-outer so each layer's operands are generated once.  Returns the per-pass
+    seconds list and the FLOP of one pass."""
+    import numpy as np  # noqa: F401
+    flops = 0
+    per_pass = [0.0] * reps
+    for li, layer in enumerate(layers):
+        sp = layer.spec if n_sample is None else layer.spec.with_batch(n_sample)
+        x, w = cpu_layer_operands(layer, sp, li)
+        for r in range(reps):
+            t0 = time.perf_counter()
+            conv(x, w, *sp.conv_args())
+            per_pass[r] += time.perf_counter() - t0
+        flops += sp.flops
+        del x, w
+    return per_pass, flops
+
+
+def run_reference_arm(args, layers, world, rank, config):
+    if rank != 0:
+        return 0
+    use_all_host_threads()
+    conv, kind, desc = cpu_impl()
+    for _ in range(args.warmup):  # warm BLAS threads and page in the code: one image per layer
+        cpu_time_layers(layers, 1, conv)
+    # one full pass first: it sizes how many of the requested passes fit the time budget
+    first, flops = cpu_time_layers(layers, None, conv)
+    steps = max(1, min(args.steps, int(args.ref_budget_s // max(first[0], 1e-9))))
+    times = first
+    if steps > 1:
+        more, _ = cpu_time_layers(layers, None, conv, reps=steps - 1)
+        times = first + more
     mean_s = sum(times) / len(times)
     value = flops / mean_s / 1e12
-    cores = cpu_threads()
+    cores = cpu_threads() if kind == "port" or layers[0].dtype != "int8" else 1
+    from oracle import ref as R
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, "sample_batch": n_sample, "layers": len(layers)},
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.config} all {len(layers)} layers at batch {n_sample} per step "
-                                   f"(fp32 BLAS tap accumulation on bf16-rounded operands)"},
+        "steps": steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64" if layers[0].dtype == "int8" else "f32",
+        "data": "synthetic", "config": config,
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+                         "sample": f"the whole {args.config} step (all {len(layers)} layers at the global batch "
+                                   f"{layers[0].spec.n}) per timed step, {steps} of {args.steps} requested steps "
+                                   f"within the {args.ref_budget_s:.0f} s budget; {desc}; bf16-rounded operands "
+                                   f"in fp32"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "steps_requested": args.steps,
+        "native_libs": sorted({ln.split()[-1] for ln in open("/proc/self/maps")
+                               if ln.rstrip().endswith(".so") and ROOT in ln}),
+        "ref_shared_objects": [os.path.relpath(p, ROOT) for p in R.shared_objects()],
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------ parity of the benchmarked outputs
+
+def verify_outputs(work, layers_full, world, rank, dev, shard_of, regen, reference_conv):
+    """After the timed region: all-gather every layer's output shards (NCCL on GPUs, gloo
+    on CPU; sharding.gather_shards) and, on rank 0, check the first and last image of every
+    rank's shard against the CPU oracle (int8: bit-exact; bf16: normalised max error <=
+    PARITY_TOL).  Mirrors the reference's verify loop (cli.py:230-248): every layer's
+    kernel output against the direct convolution.  Returns the parity dict (rank 0) or None."""
+    import numpy as np
+    import torch
+    from paper_2110_03901_b200.sharding import gather_shards
+    max_err, checked, bad = 0.0, 0, []
+    for li, (layer, sp, x, w, y) in enumerate(work):
+        n_total = layers_full[li].spec.n
+        y_full = gather_shards(y, n_total) if world > 1 else y
+        if rank != 0:
+            continue
+        wf = w.float().cpu().numpy() if layer.dtype != "int8" else w.cpu().numpy().astype(np.int64)
+        for r in range(world):
+            lo, hi = shard_of(n_total, r)
+            if hi <= lo:
+                continue
+            xr = x if r == rank else regen(layer, layers_full[li].spec.with_batch(hi - lo), li, lo)
+            for i in sorted({lo, hi - 1}):
+                xi = xr[i - lo:i - lo + 1]
+                xi = xi.float().cpu().numpy() if layer.dtype != "int8" else xi.cpu().numpy().astype(np.int64)
+                ref = np.asarray(reference_conv(xi, wf, *sp.conv_args()), dtype=np.float64)
+                got = y_full[i:i + 1].float().cpu().numpy().astype(np.float64)
+                if layer.dtype == "int8":
+                    err = 0.0 if np.array_equal(got, ref) else float("inf")
+                else:
+                    err = float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+                max_err = max(max_err, err)
+                checked += 1
+                if not err <= PARITY_TOL:
+                    bad.append(f"{layer.name}[{i}]")
+        del y_full
+    if rank != 0:
+        return None
+    return {"ok": not bad, "checked_images": checked, "layers": len(work), "max_norm_err": max_err,
+            "tol": PARITY_TOL if layers_full[0].dtype != "int8" else 0.0,
+            "bar": "bit-exact" if layers_full[0].dtype == "int8" else "max|y-ref|/max|ref| (bf16 out vs fp32 oracle)",
+            "failures": bad[:10],
+            "how": "outputs of the timed steps all-gathered over ranks (sharding.gather_shards); first and last "
+                   "image of every rank's shard vs oracle.conv2d_nhwc_taps / exact int path"}
+
+
 # ------------------------------------------------------------------ GPU arm
 
 def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=4, help="batch per layer of one --impl reference step")
-    ap.add_argument("--cpu-sample", type=int, default=32, help="batch per layer of the cpu_baseline sample")
+    ap.add_argument("--ref-budget-s", type=float, default=1000.0,
+                    help="--impl reference: time budget of the timed full-size steps (fewer steps if exceeded)")
+    ap.add_argument("--cpu-sample", type=int, default=64, help="batch per layer of the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--layers-json", default=None, help="write per-layer timings here (rank 0)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--emulate-world", type=int, default=0,
@@ -246,18 +423,28 @@ def main(argv=None):
                          "throughput, i.e. what the W-GPU run measures when every rank matches rank 0")
     args = ap.parse_args(argv)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus, argv)
+
     from paper_2110_03901_b200.workloads import baseline_configs
     layers_full = baseline_configs()[args.config]
     world, rank, local = dist_setup()
+    if world > 1 and args.gpus not in (1, world):
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} ranks", file=sys.stderr)
+    shard_world = world
+    if args.emulate_world > 1:
+        if world != 1:
+            raise SystemExit("--emulate-world is a single-process diagnostic")
+        shard_world = args.emulate_world
+    config = workload_config(args.config, layers_full, shard_world)
     if args.impl == "reference":
-        return run_reference_arm(args, layers_full, world, rank)
+        return run_reference_arm(args, layers_full, world, rank, config)
 
     import torch
     import torch.distributed as dist
     import paper_2110_03901_b200 as P
     from paper_2110_03901_b200 import _lib
     from paper_2110_03901_b200._kernels import conv_device
-    from paper_2110_03901_b200.lowering import touched_pixels
     # the weights are written once at setup, never inside the step: every conv may start
     # its filter loads before its programmatic-launch wait (IMCONV_FLAG_STATIC_FILTER)
     STATIC = _lib.FLAG_STATIC_FILTER
@@ -267,99 +454,65 @@ def main(argv=None):
     peaks, peak_kind = load_peaks()
 
     # ---- per-rank shard of every layer (contiguous images; no collective) ----
-    shard_world = world
-    if args.emulate_world > 1:
-        if world != 1:
-            raise SystemExit("--emulate-world is a single-process diagnostic")
-        shard_world = args.emulate_world
     work = []
     for li, layer in enumerate(layers_full):
         lo, hi = shard_batch(layer.spec.n, shard_world, rank)
         sp = layer.spec.with_batch(hi - lo)
-        g = torch.Generator(device=dev).manual_seed(1000 + li)
-        xs = (sp.n, sp.h_i, sp.w_i, sp.c_i)
-        ws = (sp.h_f, sp.w_f, sp.c_i, sp.c_o)
-        gw = torch.Generator(device=dev).manual_seed(2000 + li)  # identical weights on every rank
-        if layer.dtype == "int8":
-            x = torch.randint(-128, 128, xs, generator=g, device=dev, dtype=torch.int16).to(torch.int8)
-            w = torch.randint(-128, 128, ws, generator=gw, device=dev, dtype=torch.int16).to(torch.int8)
-            y = torch.empty((sp.n, sp.h_o, sp.w_o, sp.c_o), dtype=torch.int32, device=dev)
-        else:
-            x = torch.randn(xs, generator=g, device=dev, dtype=torch.float32)
-            if layer.relu_input:
-                x.clamp_(min=0)
-            w = torch.randn(ws, generator=gw, device=dev, dtype=torch.float32) * (2.0 / (sp.c_i * sp.h_f * sp.w_f)) ** 0.5
-            if layer.name == "stem":
-                x[..., 3:] = 0
-                w[:, :, 3:, :] = 0
-            x, w = x.to(torch.bfloat16), w.to(torch.bfloat16)
-            y = torch.empty((sp.n, sp.h_o, sp.w_o, sp.c_o), dtype=torch.bfloat16, device=dev)
+        x, w = make_operands(layer, sp, li, lo, dev)
+        odt = torch.int32 if layer.dtype == "int8" else torch.bfloat16
+        y = torch.empty((sp.n, sp.h_o, sp.w_o, sp.c_o), dtype=odt, device=dev)
         work.append((layer, sp, x, w, y))
     torch.cuda.synchronize()
 
-    def step():
-        for layer, sp, x, w, y in work:
-            conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC)
-
     total_flops_rank = sum(sp.flops for _, sp, *_ in work)
-    e_in = {"int8": 1}
-    bytes_alg_rank = 0
-    for layer, sp, x, w, y in work:
-        ei = e_in.get(layer.dtype, 2)
-        bytes_alg_rank += sp.n * touched_pixels(sp) * sp.c_i * ei + sp.h_f * sp.w_f * sp.c_i * sp.c_o * ei \
-            + sp.gemm_m * sp.c_o * y.element_size()
+    bytes_alg_rank = sum(bytes_alg(sp, layer.dtype, y.element_size()) for layer, sp, x, w, y in work)
 
-    # Consecutive timed steps must not find their inputs in L2: when one step's working set is
-    # below twice the L2 size (the small parity configs), the step rotates over `copies`
-    # independent sets of buffers (same values), so every step reads cold data.
-    l2_bytes = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 << 20))
-    copies = 1 if bytes_alg_rank >= 2 * l2_bytes else -(-2 * l2_bytes // max(bytes_alg_rank, 1))
+    # Consecutive timed passes must not find their inputs in L2: when one pass's working set
+    # is below twice the L2 size (the small parity configs), the captured step runs the pass
+    # over `copies` independent sets of buffers (same values), so every pass reads cold data.
+    copies = rotation_copies(layers_full, shard_world)
     work_sets = [work] + [[(layer, sp, x.clone(), w.clone(), torch.empty_like(y)) for layer, sp, x, w, y in work]
                           for _ in range(copies - 1)]
-    l2_note = (f"inputs larger than L2: every layer has its own buffers, per-step working set "
-               f"{bytes_alg_rank / 1e9:.1f} GB per GPU" if copies == 1 else
-               f"steps rotate over {copies} copies of the {bytes_alg_rank / 1e6:.1f} MB working set "
-               f"({copies * bytes_alg_rank / 1e6:.0f} MB > 2 x L2), so no step reads L2-resident inputs")
 
-    def step_set(ws):
+    def one_pass(ws):
         for layer, sp, x, w, y in ws:
             conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC)
 
-    # launches per step (our kernels only)
-    _lib.lib.imconv_reset_launch_count()
-    step()
-    torch.cuda.synchronize()
-    launches_per_step = int(_lib.lib.imconv_launch_count())
-
-    stream = torch.cuda.Stream()
-    graphs = []
-    if not args.no_graph:
-        stream.wait_stream(torch.cuda.current_stream())
+    def all_passes():
         for ws in work_sets:
-            with torch.cuda.stream(stream):
-                step_set(ws)  # warm caches outside capture
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                step_set(ws)
-            graphs.append(g)
+            one_pass(ws)
+
+    # launches per pass (our kernels only)
+    _lib.lib.imconv_reset_launch_count()
+    one_pass(work)
+    torch.cuda.synchronize()
+    launches_per_pass = int(_lib.lib.imconv_launch_count())
+
+    graph = None
+    if not args.no_graph:
+        stream = torch.cuda.Stream()
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            all_passes()  # warm caches outside capture
         torch.cuda.synchronize()
-    graph = graphs[0] if graphs else None
-    step_ctr = [0]
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            all_passes()  # one replay = `copies` passes, one per buffer set
+        torch.cuda.synchronize()
 
-    def run_step():
-        i = step_ctr[0] % copies
-        step_ctr[0] += 1
-        if graphs:
-            graphs[i].replay()
+    def run_replay():
+        if graph is not None:
+            graph.replay()
         else:
-            step_set(work_sets[i])
+            all_passes()
 
-    for _ in range(max(args.warmup, 3)):
-        run_step()
+    replays = -(-args.steps // copies)  # timed passes = replays * copies >= steps
+    passes = replays * copies
+    for _ in range(max(-(-max(args.warmup, 3) // copies), 1)):
+        run_replay()
     torch.cuda.synchronize()
 
-    # ---- timed region: K back-to-back steps ----
+    # ---- timed region: back-to-back passes ----
     sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -369,14 +522,15 @@ def main(argv=None):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     cur = torch.cuda.current_stream()
     ev0.record(cur)
-    for _ in range(args.steps):
-        run_step()
+    for _ in range(replays):
+        run_replay()
     ev1.record(cur)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    region_ms_rank = ev0.elapsed_time(ev1)
+    ms_rank = region_ms_rank / passes
     ms = ms_rank
     if world > 1:
         t = torch.tensor([ms_rank], device=dev, dtype=torch.float64)
@@ -386,6 +540,15 @@ def main(argv=None):
     if shard_world != world:  # emulated: every rank assumed as fast as rank 0
         total_flops = total_flops_rank * shard_world
     value = total_flops / (ms / 1e3) / 1e12
+
+    # ---- parity of what was just timed ----
+    parity = None
+    if not args.no_parity and shard_world == world:
+        from oracle import oracle as O
+        ref_conv = O.conv2d_nhwc_taps if layers_full[0].dtype != "int8" else O.conv2d_nhwc_exact_f64
+        parity = verify_outputs(work, layers_full, world, rank, dev,
+                                lambda n, r: shard_batch(n, world, r),
+                                lambda layer, sp, li, lo: make_operands(layer, sp, li, lo, dev)[0], ref_conv)
 
     # ---- per-layer kernel times (separate pass): each layer's `reps` launches
     # are replayed from their own CUDA graph, so host launch latency cannot
@@ -425,20 +588,22 @@ def main(argv=None):
             best = t if best is None else min(best, t)
         int8_peak = 2 * 8192 ** 3 / (best / 1e3) / 1e12
         del a8, b8
-    dtype_peak = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
+    burst = region_ms_rank < BURST_REGION_MS
+    bf16_peak = peaks.get("bf16_tflops" if burst else "bf16_tflops_sustained",
+                          PEAKS_FALLBACK["bf16_tflops" if burst else "bf16_tflops_sustained"])
+    dtype_peak = bf16_peak
     if int8_peak is not None and all(l.dtype == "int8" for l, *_ in work):
         dtype_peak = int8_peak
     hbm = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
-    # achieved: this rank's FLOP over its device time per step in the TIMED region (the step
+    # achieved: this rank's FLOP over its device time per pass in the TIMED region (the step
     # is nothing but the conv kernels); the separate per-layer pass only apportions it
     achieved = total_flops_rank / (ms_rank / 1e3) / 1e12
     roof_ms = 0.0
     layer_rows = []
     for layer, sp, t_ms in per_layer:
-        ei = e_in.get(layer.dtype, 2)
         eo = 4 if layer.dtype == "int8" else 2
-        b = sp.n * touched_pixels(sp) * sp.c_i * ei + sp.h_f * sp.w_f * sp.c_i * sp.c_o * ei + sp.gemm_m * sp.c_o * eo
-        pk = int8_peak if (layer.dtype == "int8" and int8_peak) else dtype_peak
+        b = bytes_alg(sp, layer.dtype, eo)
+        pk = int8_peak if (layer.dtype == "int8" and int8_peak) else bf16_peak
         t_roof = max(sp.flops / (pk * 1e12), b / (hbm * 1e9)) * 1e3
         roof_ms += t_roof
         layer_rows.append({"layer": layer.name, "n": sp.n, "ms": round(t_ms, 5),
@@ -487,15 +652,20 @@ def main(argv=None):
         e2e = {"value": total_flops / (e_ms / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
 
-    # ---- CPU baseline (rank 0, N=1 only) ----
+    # ---- CPU baseline (rank 0, N=1 only): the reference's kernels on a bounded sample ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        s, f = cpu_reference_step(layers_full, args.cpu_sample)
-        cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"{args.config}: all {len(layers_full)} layers at batch {args.cpu_sample} "
-                         f"(oracle port of _fallback.conv2d_nhwc, fp32 OpenBLAS, {s:.1f} s)"}
+    if rank == 0 and world == 1 and shard_world == 1 and not args.no_cpu:
+        use_all_host_threads()
+        conv, kind, desc = cpu_impl()
+        n_s = min(args.cpu_sample, layers_full[0].spec.n)
+        cpu_time_layers(layers_full[:1], 1, conv)  # warm-up
+        secs, f = cpu_time_layers(layers_full, n_s, conv)
+        cores = 1 if (layers_full[0].dtype == "int8" and kind == "reference") else cpu_threads()
+        cpu = {"value": f / secs[0] / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+               "sample": f"{args.config}: all {len(layers_full)} layers at batch {n_s} of {layers_full[0].spec.n} "
+                         f"({desc}; {secs[0]:.1f} s)"}
 
-    traffic, traffic_src = committed_traffic(args.config)
+    traffic, traffic_note = committed_traffic(args.config, shard_world)
     # the stem executes C = 8 (3 image channels zero-padded, as BASELINE.json defines it);
     # the same run with only the 3 useful channels counted
     useful_value = None
@@ -503,48 +673,50 @@ def main(argv=None):
     if stem:
         useful_value = value * (total_flops_rank - stem[0].flops * 5 / 8) / total_flops_rank
     if rank == 0:
+        peak_name = "int8 TOPS (cuBLAS torch._int_mm, this run)" if dtype_peak == int8_peak else (
+            f"{peak_kind} bf16 {'burst' if burst else 'sustained'} (MEASURED_PEAKS.json; timed region "
+            f"{region_ms_rank:.0f} ms {'<' if burst else '>='} {BURST_REGION_MS:.0f} ms)")
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": passes,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16" if args.config != "cfg5" else "int8", "data": "synthetic",
-            "config": {"workload": args.config + (" (ResNet-50 v1.5, 53 convs, 224x224)" if args.config == "cfg4" else ""),
-                       "global_batch": layers_full[0].spec.n, "per_gpu_batch": work[0][1].n,
-                       "parallelism": f"dp{world} (N-sharded, no collective)",
-                       "l2": l2_note,
-                       "cuda_graph": graph is not None,
-                       **({"value_stem_c3": useful_value} if useful_value is not None else {})},
+            "vs_baseline": None, "dtype": "bf16" if layers_full[0].dtype != "int8" else "int8", "data": "synthetic",
+            "config": config,
             **({"emulated_world": shard_world} if shard_world != world else {}),
-            "pct_of_peak": {"measured_sustained": value / shard_world / dtype_peak,
-                            "unit_peak": "int8 TOPS" if dtype_peak == int8_peak else "bf16 TFLOP/s",
-                            "measured_burst": value / shard_world / (dtype_peak if dtype_peak == int8_peak
-                                                               else peaks.get("bf16_tflops", 1648.9)),
-                            "datasheet": value / shard_world / (4500.0 if dtype_peak == int8_peak else 2250.0)},
+            "run": {"cuda_graph": graph is not None, "passes_per_replay": copies, "replays": replays,
+                    "timed_region_ms": region_ms_rank,
+                    **({"value_stem_c3": useful_value} if useful_value is not None else {})},
+            "pct_of_peak": {"measured_burst": value / shard_world / (dtype_peak if dtype_peak == int8_peak
+                                                                     else peaks.get("bf16_tflops", 1648.9)),
+                            "measured_sustained": value / shard_world / (
+                                dtype_peak if dtype_peak == int8_peak else peaks.get("bf16_tflops_sustained", 1400.0)),
+                            "datasheet": value / shard_world / (4500.0 if dtype_peak == int8_peak else 2250.0),
+                            "unit_peak": "int8 TOPS" if dtype_peak == int8_peak else "bf16 TFLOP/s"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": dtype_peak, "unit": "TFLOP/s",
                          "frac": achieved / dtype_peak,
-                         "traffic": None if traffic is None else traffic / world,
+                         "traffic": traffic,
                          "traffic_unit": "DRAM bytes per step per GPU (ncu dram__bytes_read+write)",
-                         "traffic_source": traffic_src,
+                         "traffic_source": traffic_note,
                          "bytes_alg": bytes_alg_rank,
-                         "peak_kind": (f"cuBLAS int8 (torch._int_mm 8192^3) measured in this run"
-                                       if int8_peak is not None and dtype_peak == int8_peak
-                                       else f"{peak_kind} bf16 sustained (MEASURED_PEAKS.json)"),
+                         "peak_kind": peak_name,
                          "kernel": "conv kernels (generic / row-band / halo), all layers of the step",
-                         "achieved_source": "timed region: rank FLOP / device ms per step",
+                         "achieved_source": "timed region: rank FLOP / device ms per pass",
                          "roofline_limited_frac": roof_ms / ms_rank},
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches_per_pass * passes,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
         if args.layers_json:
             with open(args.layers_json, "w") as fh:
-                json.dump({"config": args.config, "world": world, "kernel_ms": kern_ms, "roofline_ms": roof_ms,
-                           "layers": layer_rows}, fh, indent=1)
+                json.dump({"config": args.config, "world": shard_world, "kernel_ms": kern_ms,
+                           "roofline_ms": roof_ms, "layers": layer_rows}, fh, indent=1)
+    rc = 0 if (parity is None or rank != 0 or parity["ok"]) else 1
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    return 0
+    return rc
 
 
 if __name__ == "__main__":

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define IMCONV_ABI_VERSION 2
+#define IMCONV_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define IMCONV_API __attribute__((visibility("default")))
@@ -89,7 +89,14 @@ extern "C" {
  *         in = I8 -> out = I32 (int32 accumulation, bit-exact).
  * Requires c*elem % 16 == 0 and k*elem % 16 == 0 (the Python shim pads).
  * tile_n: 0 = auto, else 64/128/256 (output channels per CTA tile).
- * num_ctas: 0 = one persistent CTA per SM, else the grid size.
+ * num_ctas: 0 = one persistent CTA per SM, else the grid size.  Above the SM
+ *   count the grid is no longer co-resident, so the split-K tail (whose splits
+ *   wait for each other) is turned off for such grids.
+ * Stream capture: every call may be captured into a CUDA graph and the graph
+ *   replayed any number of times (split-K counters are monotonic tickets, the
+ *   partial-sum workspace is a stream-ordered allocation, i.e. a graph memory
+ *   node).  A captured graph must not run concurrently with another replay of
+ *   a graph captured from the same call.
  */
 typedef struct imconv_conv_args {
     const void *x;
@@ -193,6 +200,28 @@ typedef struct imconv_traffic {
 } imconv_traffic;
 IMCONV_API int imconv_predict_traffic(const imconv_conv_args *args, int64_t l2_bytes, int32_t sms,
                                       imconv_traffic *out);
+
+/*
+ * The launch imconv_conv2d_nhwc would issue for these arguments on a device
+ * with `sms` SMs (host code, no GPU, pointers ignored): which kernel, and for
+ * the generic kernel the planner's block shape, grid, CTA pairs, B-stationary
+ * and split-K decisions.  Introspection for tests and tools (the branches the
+ * benchmarked batch sizes select); same return codes as imconv_conv2d_nhwc's
+ * argument checks.
+ */
+typedef struct imconv_plan_info {
+    int32_t kernel;      /* 0 generic, 1 row-band, 2 halo, 3 halo with a streamed filter */
+    int32_t grid;        /* generic kernel: CTAs launched */
+    int32_t bn;          /* output channels per block */
+    int32_t mt;          /* 128-row m-tiles per CTA block */
+    int32_t ksub;        /* k-subtiles per pipeline stage */
+    int32_t cta_pair;    /* 1: cta_group::2 CTA pairs (256-row blocks) */
+    int32_t b_resident;  /* 1: each CTA loads its filter slice once */
+    int32_t sk_split;    /* split-K ways of the tail tiles (1 = no split) */
+    int64_t tiles;       /* output blocks */
+    int64_t sk_tail;     /* tail blocks whose k-loop is split */
+} imconv_plan_info;
+IMCONV_API int imconv_plan(const imconv_conv_args *args, int32_t sms, imconv_plan_info *out);
 
 /* Device / build introspection (no compute). */
 IMCONV_API int imconv_abi_version(void);

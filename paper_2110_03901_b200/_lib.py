@@ -1,7 +1,10 @@
 """ctypes binding of the C ABI in include/imconv.h (libimconv.so, in-tree).
 
-There is no fallback: if the shared object is missing the import fails
-loudly, and every compute call raises when no CUDA device is present.
+The shared object is mapped on first use of ``_lib.lib`` (PEP 562 module
+``__getattr__``), not at import: importing the package for its host-side
+pieces (ConvSpec, the layer tables) loads no native code.  There is no
+fallback: if the shared object is missing the first call fails loudly, and
+every compute call raises when no CUDA device is present.
 """
 
 from __future__ import annotations
@@ -10,10 +13,11 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# IMCONV_INSTRUMENTED=1 (tools/run_layer.py --waits) loads the same sources built
-# with per-role wait counters; it is not a different backend.
-LIB_PATH = os.path.join(_PKG, "libimconv_instr.so" if os.environ.get("IMCONV_INSTRUMENTED") == "1"
-                        else "libimconv.so")
+LIB_PATH = os.path.join(_PKG, "libimconv.so")
+# the same sources built with per-role wait counters (-DIMCONV_INSTRUMENT=1): loaded only
+# by diagnostic tools that ask for it explicitly (use_instrumented), never by the package
+LIB_INSTR_PATH = os.path.join(_PKG, "libimconv_instr.so")
+_loaded = None
 
 # element-type codes, include/imconv.h
 BF16, F16, I8, F32, I32 = 0, 1, 2, 3, 4
@@ -27,7 +31,7 @@ EXPORTED = (
     "imconv_conv2d_nhwc", "imconv_out_extent", "imconv_gemm", "imconv_tile_gather_nhwc",
     "imconv_im2col_nhwc", "imconv_pad_copy", "imconv_lru_simulate", "imconv_abi_version",
     "imconv_device_sm_count", "imconv_strerror", "imconv_launch_count", "imconv_reset_launch_count",
-    "imconv_debug_set_buffer", "imconv_debug_set_flags", "imconv_predict_traffic",
+    "imconv_debug_set_buffer", "imconv_debug_set_flags", "imconv_predict_traffic", "imconv_plan",
 )
 
 
@@ -59,18 +63,28 @@ class ImconvTraffic(ctypes.Structure):
     ]
 
 
+class ImconvPlanInfo(ctypes.Structure):
+    """Mirror of imconv_plan_info (include/imconv.h)."""
+
+    _fields_ = [
+        ("kernel", ctypes.c_int32), ("grid", ctypes.c_int32), ("bn", ctypes.c_int32), ("mt", ctypes.c_int32),
+        ("ksub", ctypes.c_int32), ("cta_pair", ctypes.c_int32), ("b_resident", ctypes.c_int32),
+        ("sk_split", ctypes.c_int32), ("tiles", ctypes.c_int64), ("sk_tail", ctypes.c_int64),
+    ]
+
+
 class ImconvError(RuntimeError):
     def __init__(self, code: int, what: str):
         self.code = code
         super().__init__(f"{what}: {strerror(code)} (code {code})")
 
 
-def _load():
-    if not os.path.exists(LIB_PATH):
+def _load(path: str):
+    if not os.path.exists(path):
         raise ImportError(
-            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
             "(there is no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     L.imconv_conv2d_nhwc.argtypes = [ctypes.POINTER(ImconvArgs), vp]
     L.imconv_conv2d_nhwc.restype = ctypes.c_int
@@ -102,13 +116,29 @@ def _load():
     L.imconv_debug_set_flags.restype = None
     L.imconv_predict_traffic.argtypes = [ctypes.POINTER(ImconvArgs), i64, i32, ctypes.POINTER(ImconvTraffic)]
     L.imconv_predict_traffic.restype = ctypes.c_int
+    L.imconv_plan.argtypes = [ctypes.POINTER(ImconvArgs), i32, ctypes.POINTER(ImconvPlanInfo)]
+    L.imconv_plan.restype = ctypes.c_int
     return L
 
 
-lib = _load()
-# experiment switches (A/B measurements only): host-side debug flags of the C ABI
-if os.environ.get("IMCONV_DEBUG_FLAGS"):
-    lib.imconv_debug_set_flags(int(os.environ["IMCONV_DEBUG_FLAGS"], 0))
+def use_instrumented() -> None:
+    """Diagnostics only (tools/run_layer.py --waits, tools/timeline_probe.py): bind the
+    instrumented build instead of the product library.  Must precede any other use."""
+    global _loaded
+    if _loaded is not None and _loaded[0] != LIB_INSTR_PATH:
+        raise RuntimeError("libimconv.so is already loaded in this process")
+    _loaded = (LIB_INSTR_PATH, _load(LIB_INSTR_PATH))
+    globals()["lib"] = _loaded[1]
+
+
+def __getattr__(name):
+    global _loaded
+    if name == "lib":
+        if _loaded is None:
+            _loaded = (LIB_PATH, _load(LIB_PATH))
+        globals()["lib"] = _loaded[1]
+        return _loaded[1]
+    raise AttributeError(name)
 
 
 def strerror(code: int) -> str:

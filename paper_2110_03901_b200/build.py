@@ -9,6 +9,7 @@ include/imconv.h) on a machine without a GPU.
 
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -19,7 +20,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libimconv.so")
 LIB_INSTR = os.path.join(PKG, "libimconv_instr.so")  # same sources, -DIMCONV_INSTRUMENT=1 (tools only)
 SOURCES = [os.path.join(CSRC, f) for f in ("imconv_api.cu", "lru.cpp")]
-HEADERS = [os.path.join(CSRC, f) for f in ("ptx.cuh", "conv_kernel.cuh", "conv_rowband.cuh", "conv_halo.cuh", "aux_kernels.cuh")] + [
+# every header the sources can include: a stale .so must never survive an edit to one of them
+HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) + [
     os.path.join(ROOT, "include", "imconv.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

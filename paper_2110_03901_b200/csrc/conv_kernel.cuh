@@ -76,8 +76,7 @@ struct ConvParams {
     int sk_split;        // split-K tail: S > 1 splits each of the last (total - sk_first) tiles' k-loop S ways
     long long sk_first;  // first tail tile (a multiple of the grid: the full waves end here)
     float *sk_ws;        // fp32 partials [tail tile][S][MT*128 rows][BN]
-    unsigned long long *sk_cnt;  // per tail tile arrival counters, tagged (sk_gen << 8) | count
-    unsigned long long sk_gen;   // launch generation (counters never need clearing)
+    unsigned long long *sk_cnt;  // per tail tile ticket counters (monotonic, see sk_arrive)
     int b_resident;      // 1: grid is a multiple of n_tiles (each CTA keeps one output-channel block) --
                          //    when a block's k-subtiles fit the B ring, its filter slice is loaded once
     int a_cl;            // 1: channel-last baseline -- reduction order k = (c*R + r)*S + s, A gathered
@@ -149,17 +148,21 @@ __device__ __forceinline__ bool get_unit(long long u, long long full_end, long l
     return true;
 }
 
-// Arrival of one split on its tail tile's counter; true for the last (S-th)
-// arrival of this launch.  Counters are tagged with the launch generation, so
-// a stale value from an earlier launch restarts the count at 1.
-__device__ __forceinline__ bool sk_arrive(unsigned long long *slot, unsigned long long gen, int S) {
-    unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(slot);
-    while (true) {
-        const unsigned long long nv = (cur >> 8) == gen ? cur + 1 : ((gen << 8) | 1ull);
-        const unsigned long long prev = atomicCAS(slot, cur, nv);
-        if (prev == cur) return static_cast<int>(nv & 0xff) == S;
-        cur = prev;
-    }
+// Arrival of one split on its tail tile's ticket counter.  Counters only grow:
+// between launches a slot holds a multiple of kSkRound; inside a launch each of
+// the S (<= 5) splits adds 1 and the split that completes the set rounds the slot
+// up to the next multiple.  Nothing is ever cleared and no launch-specific value
+// is baked into the parameters, so a CUDA graph replaying the same launch again
+// and again (bench.py's timed step) sees a fresh count every time.  Returns the
+// value that proves all S splits of THIS launch have arrived; `last` is set for
+// the completing arrival.
+constexpr unsigned long long kSkRound = 64;
+__device__ __forceinline__ unsigned long long sk_arrive(unsigned long long *slot, int S, bool &last) {
+    const unsigned long long old = atomicAdd(slot, 1ull);
+    const unsigned long long base = old & ~(kSkRound - 1);
+    last = old - base == static_cast<unsigned long long>(S - 1);
+    if (last) atomicAdd(slot, kSkRound - static_cast<unsigned long long>(S));
+    return base + static_cast<unsigned long long>(S);
 }
 
 // Instrumentation (IMCONV_INSTRUMENT builds only, libimconv_instr.so): cycles
@@ -917,13 +920,14 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                     // arrive, then wait for the tile's other splits (all co-resident: the tail
                     // units are the last unit of distinct persistent CTAs)
                     unsigned long long *slot = p.sk_cnt + tt;
-                    if (!sk_arrive(slot, p.sk_gen, S)) {
+                    bool last = false;
+                    const unsigned long long target = sk_arrive(slot, S, last);
+                    if (!last) {
                         const long long t0 = clock64();
                         uint32_t tries = 0;
-                        while (true) {
-                            const unsigned long long c = ptx::ld_acquire_gpu(slot);
-                            if ((c >> 8) == p.sk_gen && static_cast<int>(c & 0xff) >= S) break;
+                        while (ptx::ld_acquire_gpu(slot) < target) {
                             __nanosleep(64);
+                            // a peer that never arrives is a planner bug (non-resident split): fail loudly
                             if ((++tries & 1023u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
                         }
                     }

@@ -43,25 +43,56 @@ constexpr int kDbgNoHaloStack = 1 << 25;  // halo kernel: one sub-block per bloc
 constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep the generic kernel
 constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-stationary layout
 
-// Split-K arrival counters: one per tail tile, tagged with a launch generation
-// so they never need clearing; each launch uses one of 256 slices (so up to
-// 256 launches may be in flight on different streams without sharing one).
+// Split-K ticket counters (conv_kernel.cuh sk_arrive): one per tail tile, never
+// cleared (they only grow, in steps that leave a multiple of kSkRound between
+// launches).  Each launch takes one of kSkSlices slices round-robin, so launches
+// in flight at the same time on different streams do not share a counter.  The
+// counters are allocated and zeroed on first use of a device; that first use may
+// happen while the caller's stream is being captured into a CUDA graph, so the
+// allocation runs in relaxed capture mode and the zeroing on a private stream
+// that is not part of any capture.
 std::mutex g_sk_mutex;
 unsigned long long *g_sk_counters[64] = {};
-std::atomic<unsigned long long> g_sk_gen{1};
+std::atomic<unsigned long long> g_sk_slice{0};
 constexpr int kSkSlices = 256, kSkSliceLen = 256;
 
 unsigned long long *sk_counters(int dev) {
     std::lock_guard<std::mutex> lock(g_sk_mutex);
     if (dev < 0 || dev >= 64) return nullptr;
     if (!g_sk_counters[dev]) {
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        cudaThreadExchangeStreamCaptureMode(&mode);
         void *ptr = nullptr;
+        cudaStream_t zs = nullptr;
         const size_t bytes = sizeof(unsigned long long) * kSkSlices * kSkSliceLen;
-        if (cudaMalloc(&ptr, bytes) != cudaSuccess) return nullptr;
-        if (cudaMemset(ptr, 0, bytes) != cudaSuccess) return nullptr;
+        bool ok = cudaMalloc(&ptr, bytes) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&zs, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaMemsetAsync(ptr, 0, bytes, zs) == cudaSuccess && cudaStreamSynchronize(zs) == cudaSuccess;
+        if (zs) cudaStreamDestroy(zs);
+        if (!ok && ptr) cudaFree(ptr);
+        cudaThreadExchangeStreamCaptureMode(&mode);  // restore the caller's mode
+        if (!ok) {
+            cudaGetLastError();
+            return nullptr;
+        }
         g_sk_counters[dev] = static_cast<unsigned long long *>(ptr);
     }
     return g_sk_counters[dev];
+}
+
+// cudaFuncSetAttribute is per device: each kernel instantiation keeps a bitmask of
+// the devices it has been configured on (a process may drive several GPUs).
+template <typename Kern>
+cudaError_t ensure_attrs(std::atomic<unsigned long long> &done, Kern kern, int smem, bool cluster) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess && cluster) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
 }
 
 std::mutex g_mu;
@@ -155,13 +186,8 @@ int launch_conv(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap 
                 cudaStream_t st) {
     using Cfg = ConvCfg<ELEM, OUT, BN, STAGES, KSUB, MT, CG>;
     auto kern = conv_fwd_kernel<ELEM, OUT, BN, STAGES, KSUB, MT, CG>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-        if (attr_err == cudaSuccess && CG == 2)
-            attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    });
+    static std::atomic<unsigned long long> attr_done{0};
+    const cudaError_t attr_err = ensure_attrs(attr_done, kern, Cfg::kSmemBytes, CG == 2);
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
     const int g = CG == 1 ? grid : (grid & ~1);
     cudaError_t le = launch_pdl(kern, g, kThreadsGeneric, Cfg::kSmemBytes, st, CG, ta, tb, ty, p);
@@ -234,11 +260,8 @@ template <int ELEM, int OUT, int BN, int TP, int NP, int STEM = 0>
 int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandParams &p, int smem, int grid,
                    cudaStream_t st) {
     auto kern = conv_rowband_kernel<ELEM, OUT, BN, TP, NP, STEM>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-    });
+    static std::atomic<unsigned long long> attr_done{0};
+    const cudaError_t attr_err = ensure_attrs(attr_done, kern, kMaxDynSmem, false);
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
     cudaError_t le = launch_pdl(kern, grid, kThreadsRowband, smem, st, 1, tw, ty, p);
     if (le != cudaSuccess) return static_cast<int>(le);
@@ -253,11 +276,8 @@ template <int ELEM, int OUT, int BN, int HB = 1>
 int launch_halo(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const HaloParams &p, int smem,
                 int grid, cudaStream_t st) {
     auto kern = conv_halo_kernel<ELEM, OUT, BN, HB>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-    });
+    static std::atomic<unsigned long long> attr_done{0};
+    const cudaError_t attr_err = ensure_attrs(attr_done, kern, kMaxDynSmem, false);
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
     cudaError_t le = launch_pdl(kern, grid, kThreadsGeneric, smem, st, 1, ta, tb, ty, p);
     if (le != cudaSuccess) return static_cast<int>(le);
@@ -269,7 +289,7 @@ int launch_halo(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap 
 // Halo-tile path (conv_halo.cuh): stride 1, one 128-byte swizzle row per pixel
 // (bf16/fp16 C = 64, int8 C = 128), K = BN in {64,128,256} with the whole
 // filter resident in shared memory.  Returns kNotApplicable otherwise.
-int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st) {
+int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st, bool dry = false) {
     const int E = elem_bytes(a->in_dtype);
     if (a->c * E != 128 || a->stride_h != 1 || a->stride_w != 1) return kNotApplicable;
     if (a->tile_n != 0 || a->order == IMCONV_ORDER_FILTER_MAJOR) return kNotApplicable;
@@ -314,6 +334,7 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
     if (p.n_stages < 2) return kNotApplicable;
     const int smem = fixed + p.n_stages * p.a_stage_bytes;
 
+    if (dry) return 0;  // imconv_plan: applicable, nothing encoded or launched
     CUtensorMap ta, tb, ty;
     std::memset(&ta, 0, sizeof(ta));
     std::memset(&tb, 0, sizeof(tb));
@@ -389,11 +410,8 @@ template <int ELEM, int OUT, int BN>
 int launch_halo_stream(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const HaloStreamParams &p,
                        int smem, int grid, cudaStream_t st) {
     auto kern = conv_halo_stream_kernel<ELEM, OUT, BN, 2>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-    });
+    static std::atomic<unsigned long long> attr_done{0};
+    const cudaError_t attr_err = ensure_attrs(attr_done, kern, kMaxDynSmem, false);
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
     cudaError_t le = launch_pdl(kern, grid, kThreadsGeneric, smem, st, 1, ta, tb, ty, p);
     if (le != cudaSuccess) return static_cast<int>(le);
@@ -424,7 +442,7 @@ inline bool halo_stream_wave_ok(long long halo_tiles, int64_t M, int sms) {
     return 100 * wh <= 123 * wg;
 }
 
-int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st) {
+int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st, bool dry = false) {
     const int E = elem_bytes(a->in_dtype);
     if (E != 2 || a->stride_h != 1 || a->stride_w != 1) return kNotApplicable;
     if (a->c * E <= 128 || (a->c * E) % 128 != 0) return kNotApplicable;
@@ -469,6 +487,7 @@ int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cu
     if (p.nb < 3) return kNotApplicable;
     const int smem = fixed + p.na * p.a_slot_bytes + p.nb * b_stage;
 
+    if (dry) return 0;  // imconv_plan: applicable, nothing encoded or launched
     CUtensorMap ta, tb, ty;
     std::memset(&ta, 0, sizeof(ta));
     std::memset(&tb, 0, sizeof(tb));
@@ -532,7 +551,7 @@ int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cu
 
 // Row-band path for 16-byte pixels (bf16/fp16, C = 8).  Returns kNotApplicable
 // when the layer does not qualify (the caller then uses the generic kernel).
-int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st) {
+int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st, bool dry = false) {
     if (!(a->in_dtype == IMCONV_BF16 || a->in_dtype == IMCONV_F16) || a->c != 8) return kNotApplicable;
     if (a->tile_n != 0 || a->k > 256 || a->s > 2 * kMaxPairs || a->stride_w > 8) return kNotApplicable;
     const int K = static_cast<int>(a->k), R = static_cast<int>(a->r), S = static_cast<int>(a->s);
@@ -623,6 +642,7 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
         return kNotApplicable;
     const int smem = fixed + p.n_stages * p.a_stage_bytes;
 
+    if (dry) return 0;  // imconv_plan: applicable, nothing encoded or launched
     CUtensorMap tw, ty;
     std::memset(&tw, 0, sizeof(tw));
     std::memset(&ty, 0, sizeof(ty));
@@ -846,7 +866,9 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
     // keeps >= 4 pipeline stages; S <= 5 so S peer blocks fit the idle operand ring.
     g->sk_split = 1;
     g->sk_tail = 0;
-    if (!cl && !g->use_pair && !a_gather && !g->b_resident && !(g_debug_flags & kDbgNoSplitK)) {
+    // Splits of one tile spin-wait for each other, so every CTA of the grid must be
+    // resident at once: never with a caller grid above one CTA per SM.
+    if (!cl && !g->use_pair && !a_gather && !g->b_resident && grid <= sms && !(g_debug_flags & kDbgNoSplitK)) {
         const int k_st = (g->k_subs + g->ksub - 1) / g->ksub;
         const long long g0 = grid;
         const long long tail = g->tiles >= g0 ? g->tiles % g0 : g->tiles;
@@ -862,7 +884,8 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
             // and only when the stages saved (k_st * (1 - 1/S) at ~600 cycles) beat the
             // ~15k-cycle partial round trip: a 3-way split of a 36-stage tail loses
             // (s4 3x3 at N = 128: 31.6 us split vs 29.3 us with CTA pairs)
-            if (Sk >= 2 && static_cast<long long>(k_st) * (Sk - 1) > static_cast<long long>(kSkCyclesPerSplit / 600) * Sk) {
+            if (Sk >= 2 && tail <= kSkSliceLen &&
+                static_cast<long long>(k_st) * (Sk - 1) > static_cast<long long>(kSkCyclesPerSplit / 600) * Sk) {
                 g->sk_split = Sk;
                 g->sk_tail = tail;
                 if (g->tiles < g0) grid = static_cast<int>(tail * Sk);
@@ -1115,10 +1138,12 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
     return 0;
 }
 
-extern "C" {
-
-int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
-    if (!a || !a->x || !a->w || !a->y) return IMCONV_EINVAL;
+// Argument checks shared by imconv_conv2d_nhwc and imconv_plan (the reference
+// validates in ConvSpec.__post_init__, core.py:72-87; the kernel level adds the
+// dtype, 16-byte and TMA im2col limits).
+static int validate_conv_args(const imconv_conv_args *a, int64_t *P_out, int64_t *Q_out, bool need_ptrs) {
+    if (!a) return IMCONV_EINVAL;
+    if (need_ptrs && (!a->x || !a->w || !a->y)) return IMCONV_EINVAL;
     const int64_t N = a->n, H = a->h, W = a->w_, C = a->c, K = a->k, R = a->r, S = a->s;
     if (N < 1 || H < 1 || W < 1 || C < 1 || K < 1 || R < 1 || S < 1) return IMCONV_EINVAL;
     if (a->stride_h < 1 || a->stride_w < 1 || a->dil_h < 1 || a->dil_w < 1 || a->pad_h < 0 || a->pad_w < 0)
@@ -1126,15 +1151,14 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     const int64_t P = imconv_out_extent(H, R, a->stride_h, a->pad_h, a->dil_h);
     const int64_t Q = imconv_out_extent(W, S, a->stride_w, a->pad_w, a->dil_w);
     if (P < 1 || Q < 1) return IMCONV_EINVAL;
-
     const bool f16in = a->in_dtype == IMCONV_BF16 || a->in_dtype == IMCONV_F16;
     if (!(f16in && (a->out_dtype == a->in_dtype || a->out_dtype == IMCONV_F32)) &&
         !(a->in_dtype == IMCONV_I8 && a->out_dtype == IMCONV_I32))
         return IMCONV_EDTYPE;
+    if ((a->flags & IMCONV_FLAG_CHANNEL_LAST) && !f16in) return IMCONV_EDTYPE;
     const int E = elem_bytes(a->in_dtype);
     if ((C * E) % 16 != 0 || (K * E) % 16 != 0) return IMCONV_ECHAN;
-    if (!aligned16(a->x) || !aligned16(a->w) || !aligned16(a->y)) return IMCONV_EALIGN;
-
+    if (need_ptrs && (!aligned16(a->x) || !aligned16(a->w) || !aligned16(a->y))) return IMCONV_EALIGN;
     // TMA im2col limits for a 4-D tensor: corners in [-128,127], tap offsets
     // in [0,255], traversal stride <= 8, dims < 2^32.
     const int64_t lo_w = -a->pad_w, lo_h = -a->pad_h;
@@ -1146,30 +1170,96 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     if (a->stride_h > 8 || a->stride_w > 8) return IMCONV_ERANGE;
     const int64_t M = N * P * Q;
     if (M >= (1ll << 31) || R * S * C >= (1ll << 31) || H * W >= (1ll << 31)) return IMCONV_ERANGE;
+    *P_out = P;
+    *Q_out = Q;
+    return 0;
+}
 
-    int rc = load_driver_entry_points();
+// The specialised kernels, in the order imconv_conv2d_nhwc tries them (shared with
+// imconv_plan, which asks the same questions with dry = true):
+//   16-byte pixels -> the row-band kernel (unless the generic kernel's cp.async tap
+//   gathers are requested; measured 0.47 vs 0.94 ms on the ResNet stem);
+//   128-byte pixels, stride 1, filter resident in smem -> halo tiles (each input
+//   pixel enters shared memory once per block, taps are descriptor offsets);
+//   multi-chunk 16-bit pixels, stride 1, K <= 128 -> halo tiles with a streamed filter.
+// Returns kNotApplicable when the generic kernel runs; *kernel = 1/2/3 otherwise.
+static int route_special(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStream_t st, bool dry,
+                         int *kernel) {
+    const bool cl = (a->flags & IMCONV_FLAG_CHANNEL_LAST) != 0;
+    *kernel = 0;
+    if (!cl && !(a->flags & IMCONV_FLAG_GATHER16) && a->order != IMCONV_ORDER_FILTER_MAJOR) {
+        const int rb = try_rowband(a, P, Q, sms, st, dry);
+        if (rb != kNotApplicable) {
+            *kernel = 1;
+            return rb;
+        }
+    }
+    if (!cl && !(a->flags & IMCONV_FLAG_NO_HALO)) {
+        const int hr = try_halo(a, P, Q, sms, st, dry);
+        if (hr != kNotApplicable) {
+            *kernel = 2;
+            return hr;
+        }
+        const int hs = try_halo_stream(a, P, Q, sms, st, dry);
+        if (hs != kNotApplicable) {
+            *kernel = 3;
+            return hs;
+        }
+    }
+    return kNotApplicable;
+}
+
+extern "C" int imconv_plan(const imconv_conv_args *a, int32_t sms, imconv_plan_info *out) {
+    if (!a || !out || sms < 1) return IMCONV_EINVAL;
+    int64_t P = 0, Q = 0;
+    int rc = validate_conv_args(a, &P, &Q, false);
+    if (rc) return rc;
+    std::memset(out, 0, sizeof(*out));
+    int kernel = 0;
+    if (route_special(a, P, Q, sms, nullptr, true, &kernel) != kNotApplicable) {
+        out->kernel = kernel;
+        out->sk_split = 1;
+        return 0;
+    }
+    GenericPlan g;
+    rc = plan_generic(a, P, Q, sms, &g);
+    if (rc) return rc;
+    out->kernel = 0;
+    out->grid = g.grid;
+    out->bn = g.bn;
+    out->mt = g.mt;
+    out->ksub = g.ksub;
+    out->cta_pair = g.use_pair ? 1 : 0;
+    out->b_resident = g.b_resident ? 1 : 0;
+    out->sk_split = g.sk_split;
+    out->tiles = g.tiles;
+    out->sk_tail = g.sk_tail;
+    return 0;
+}
+
+extern "C" {
+
+int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
+    int64_t P = 0, Q = 0;
+    int rc = validate_conv_args(a, &P, &Q, true);
+    if (rc) return rc;
+    const int64_t N = a->n, H = a->h, W = a->w_, C = a->c, K = a->k, R = a->r, S = a->s;
+    const int E = elem_bytes(a->in_dtype);
+    const int64_t lo_w = -a->pad_w, lo_h = -a->pad_h;
+    const int64_t up_w = a->pad_w - static_cast<int64_t>(a->dil_w) * (S - 1);
+    const int64_t up_h = a->pad_h - static_cast<int64_t>(a->dil_h) * (R - 1);
+    const int64_t M = N * P * Q;
+
+    rc = load_driver_entry_points();
     if (rc) return rc;
     int sms = 0;
     rc = sm_count_for_current_device(&sms);
     if (rc) return rc;
 
-    // 16-byte pixels: the row-band kernel unless the generic kernel's cp.async
-    // tap gathers are requested (measured 0.47 vs 0.94 ms on the ResNet stem)
-    const bool cl = (a->flags & IMCONV_FLAG_CHANNEL_LAST) != 0;
-    if (cl && !f16in) return IMCONV_EDTYPE;  // (the channel-last baseline gathers 2-byte elements)
-    if (!cl && !(a->flags & IMCONV_FLAG_GATHER16) && a->order != IMCONV_ORDER_FILTER_MAJOR) {
-        const int rb = try_rowband(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
-        if (rb != kNotApplicable) return rb;
-    }
-
-    // 128-byte pixels, stride 1, filter resident in smem: halo tiles (each
-    // input pixel enters shared memory once per block, taps are descriptor offsets)
-    if (!cl && !(a->flags & IMCONV_FLAG_NO_HALO)) {
-        const int hr = try_halo(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
-        if (hr != kNotApplicable) return hr;
-        const int hs = try_halo_stream(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream));
-        if (hs != kNotApplicable) return hs;
-    }
+    const bool cl = (a->flags & IMCONV_FLAG_CHANNEL_LAST) != 0;  // (2-byte elements only: validated)
+    int kernel = 0;
+    const int sp = route_special(a, P, Q, sms, reinterpret_cast<cudaStream_t>(stream), false, &kernel);
+    if (sp != kNotApplicable) return sp;
 
     GenericPlan plan;
     rc = plan_generic(a, P, Q, sms, &plan);
@@ -1361,12 +1451,11 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         unsigned long long *cnt = sk_counters(dev);
         const size_t ws_bytes = static_cast<size_t>(plan.sk_tail) * plan.sk_split * (kBM * mt) * bn * 4;
         if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
-            const unsigned long long gen = g_sk_gen.fetch_add(1);
+            const unsigned long long slice = g_sk_slice.fetch_add(1) % kSkSlices;
             p.sk_split = plan.sk_split;
             p.sk_first = tiles - plan.sk_tail;
             p.sk_ws = static_cast<float *>(sk_ws);
-            p.sk_gen = gen;
-            p.sk_cnt = cnt + (gen % kSkSlices) * kSkSliceLen;
+            p.sk_cnt = cnt + slice * kSkSliceLen;
         } else {
             sk_ws = nullptr;
             cudaGetLastError();  // (allocation failure: run without splitting)

@@ -40,13 +40,39 @@ class TrafficPrediction:
     kernel: str                     # kernel conv2d_nhwc picks (the replay models the generic raster)
 
 
-def predict(spec: ConvSpec, dtype: str = "bf16", order: str = "reuse_aware", l2_bytes: int = L2_BYTES_B200,
-            sms: int = 148, out_dtype: str | None = None, flags: int = 0) -> TrafficPrediction:
-    """Predicted DRAM traffic of one ``conv2d_nhwc`` launch of ``spec``.
+@dataclass(frozen=True)
+class LaunchPlan:
+    """What imconv_conv2d_nhwc launches for one layer (imconv_plan)."""
 
-    ``dtype`` is the compute type (bf16 / f16 / int8); channels are padded the
-    way the device path pads them (16-byte rows).
-    """
+    kernel: str
+    grid: int
+    bn: int
+    mt: int
+    ksub: int
+    cta_pair: bool
+    b_resident: bool
+    sk_split: int
+    tiles: int
+    sk_tail: int
+
+    @property
+    def branch(self) -> str:
+        """Short label of the planner branch (tests and tools group layers by it)."""
+        if self.kernel != "generic":
+            return self.kernel
+        parts = [f"{128 * self.mt * (2 if self.cta_pair else 1)}x{self.bn}"]
+        if self.cta_pair:
+            parts.append("pair")
+        if self.b_resident:
+            parts.append("b-stationary")
+        if self.sk_split > 1:
+            parts.append(f"split{self.sk_split}")
+        if self.ksub > 1:
+            parts.append(f"ksub{self.ksub}")
+        return "generic " + " ".join(parts)
+
+
+def _args(spec: ConvSpec, dtype: str, out_dtype: str | None, order: str, flags: int):
     from ._device import aligned_channels, aligned_k
     in_code = {"bf16": _lib.BF16, "f16": _lib.F16, "int8": _lib.I8}[dtype]
     e = 1 if dtype == "int8" else 2
@@ -61,6 +87,27 @@ def predict(spec: ConvSpec, dtype: str = "bf16", order: str = "reuse_aware", l2_
     a.stride_h, a.stride_w, a.pad_h, a.pad_w, a.dil_h, a.dil_w = spec.conv_args()
     a.order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[order]
     a.flags = flags
+    return a
+
+
+def plan(spec: ConvSpec, dtype: str = "bf16", sms: int = 148, out_dtype: str | None = None, flags: int = 0,
+         order: str = "reuse_aware") -> LaunchPlan:
+    """The launch ``conv2d_nhwc`` issues for ``spec`` on a ``sms``-SM device (host code)."""
+    a = _args(spec, dtype, out_dtype, order, flags)
+    t = _lib.ImconvPlanInfo()
+    _lib.check(_lib.lib.imconv_plan(ctypes.byref(a), int(sms), ctypes.byref(t)), "imconv_plan")
+    return LaunchPlan(KERNELS.get(t.kernel, "?"), t.grid, t.bn, t.mt, t.ksub, bool(t.cta_pair), bool(t.b_resident),
+                      t.sk_split, t.tiles, t.sk_tail)
+
+
+def predict(spec: ConvSpec, dtype: str = "bf16", order: str = "reuse_aware", l2_bytes: int = L2_BYTES_B200,
+            sms: int = 148, out_dtype: str | None = None, flags: int = 0) -> TrafficPrediction:
+    """Predicted DRAM traffic of one ``conv2d_nhwc`` launch of ``spec``.
+
+    ``dtype`` is the compute type (bf16 / f16 / int8); channels are padded the
+    way the device path pads them (16-byte rows).
+    """
+    a = _args(spec, dtype, out_dtype, order, flags)
     t = _lib.ImconvTraffic()
     _lib.check(_lib.lib.imconv_predict_traffic(ctypes.byref(a), int(l2_bytes), int(sms), ctypes.byref(t)),
                "imconv_predict_traffic")

@@ -92,3 +92,43 @@ def test_paper_known_answers():
     # all-ones 3x3 window = 9 (tests/test_core.py:34-40)
     y = O.conv2d_nhwc_i64(np.ones((1, 3, 3, 1), np.int64), np.ones((3, 3, 1, 1), np.int64), 1, 1, 0, 0, 1, 1)
     assert y.tolist() == [[[[9]]]]
+
+
+# ---- the reference's own kernels compiled from its sources (oracle/_ref, oracle/build_ref.py) ----
+
+def _ref_or_skip():
+    from oracle import ref as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built (python oracle/build_ref.py; needs /root/reference)")
+    return R
+
+
+def test_compiled_reference_matches_golden(golden):
+    """The compiled reference reproduces its own recorded outputs: ints bit-exact through
+    _native (int64), floats through _fallback."""
+    R = _ref_or_skip()
+    for i in range(int(golden["n_int"])):
+        spec = spec_from_vec(golden[f"int{i}_spec"])
+        y = R.conv2d_nhwc(golden[f"int{i}_x"], golden[f"int{i}_w"], *conv_args(spec))
+        assert y.dtype == np.int64 and np.array_equal(y, golden[f"int{i}_y"].astype(np.int64)), i
+    for i in range(int(golden["n_flt"])):
+        spec = spec_from_vec(golden[f"flt{i}_spec"])
+        y = R.conv2d_nhwc(golden[f"flt{i}_x"], golden[f"flt{i}_w"], *conv_args(spec))
+        assert np.array_equal(y, golden[f"flt{i}_y"]), i
+
+
+def test_restatement_matches_compiled_reference(rng):
+    """oracle.conv2d_nhwc_taps (the numpy restatement) against the compiled _fallback on the
+    bench's kind of operands (strided, padded, dilated, fp32): identical tap order, so equal
+    up to BLAS blocking differences."""
+    R = _ref_or_skip()
+    for args, xs, ws in [((2, 2, 3, 3, 1, 1), (2, 30, 30, 8), (7, 7, 8, 16)),
+                         ((1, 1, 2, 2, 2, 2), (2, 12, 12, 32), (3, 3, 32, 24)),
+                         ((2, 1, 0, 1, 1, 2), (3, 9, 11, 16), (1, 3, 16, 8))]:
+        x = rng.standard_normal(xs).astype(np.float32)
+        w = rng.standard_normal(ws).astype(np.float32)
+        np.testing.assert_allclose(O.conv2d_nhwc_taps(x, w, *args), R.conv2d_nhwc(x, w, *args),
+                                   rtol=1e-5, atol=1e-5)
+        xi = rng.integers(-128, 128, size=xs).astype(np.int64)
+        wi = rng.integers(-128, 128, size=ws).astype(np.int64)
+        assert np.array_equal(O.conv2d_nhwc_i64(xi, wi, *args), R.conv2d_nhwc(xi, wi, *args))

@@ -101,3 +101,28 @@ def test_invalid_arguments():
     assert _lib.lib.imconv_predict_traffic(ctypes.byref(a), 1 << 20, 148, ctypes.byref(t)) == -1  # zero extents
     with pytest.raises(_lib.ImconvError):
         predict(ConvSpec.square(1, 64, 8, 64, 3), sms=0)
+
+
+def test_launch_plan_branches_of_the_benchmarked_batches():
+    """imconv_plan (host code): the planner branches bench.py's shards select, which the GPU
+    tests in test_gpu_bench_batches.py then check against the oracle."""
+    from paper_2110_03901_b200.traffic import plan
+    from paper_2110_03901_b200.workloads import resnet50_layers
+    by_name = {n: {l.name: plan(l.spec) for l in resnet50_layers(n)} for n in (256, 32)}
+    assert by_name[256]["stem"].kernel == "row-band"
+    assert by_name[256]["s2b0_3x3"].kernel == "halo"
+    assert by_name[256]["s3b1_3x3"].kernel == "halo-stream"
+    s5 = by_name[256]["s5b0_3x3"]
+    assert s5.kernel == "generic" and s5.sk_split == 3 and s5.sk_tail == 196 % 148
+    assert by_name[256]["s4b0_3x3"].cta_pair
+    assert by_name[32]["s5b0_3x3"].sk_split == 5
+    # a caller grid above one CTA per SM turns split-K off (splits must be co-resident)
+    from paper_2110_03901_b200 import _lib
+    from paper_2110_03901_b200.traffic import _args
+    import ctypes
+    sp = resnet50_layers(32)[-2].spec
+    a = _args(sp, "bf16", None, "reuse_aware", 0)
+    a.num_ctas = 300
+    t = _lib.ImconvPlanInfo()
+    assert _lib.lib.imconv_plan(ctypes.byref(a), 148, ctypes.byref(t)) == 0
+    assert t.sk_split == 1

@@ -23,13 +23,14 @@ def main():
     ap.add_argument("--waits", action="store_true", help="print per-role wait-cycle instrumentation")
     ap.add_argument("--dbg-flags", type=int, default=0, help="instrumentation: disable kernel roles (wrong results)")
     ap.add_argument("--once", action="store_true", help="one launch, no timing (for ncu --set full)")
+    ap.add_argument("--host-flags", type=lambda v: int(v, 0), default=0,
+                    help="host-side A/B switches of imconv_debug_set_flags (bits 16+, experiments only)")
     ap.add_argument("--rps", type=int, default=0, help="row-band kernel: input rows per stage override (0 = auto)")
     args = ap.parse_args()
-    if args.waits or args.dbg_flags:
-        os.environ["IMCONV_INSTRUMENTED"] = "1"
-
     import torch
     from paper_2110_03901_b200 import _lib
+    if args.waits or args.dbg_flags:
+        _lib.use_instrumented()
     from paper_2110_03901_b200._kernels import conv_device, gemm_device
     from paper_2110_03901_b200.workloads import baseline_configs
     import paper_2110_03901_b200._kernels as K
@@ -55,7 +56,7 @@ def run_one(args, layer):
         x = torch.randn((sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev).to(torch.bfloat16)
         w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev) * 0.05).to(torch.bfloat16)
     order = {"reuse_aware": _lib.ORDER_REUSE_AWARE, "filter_major": _lib.ORDER_FILTER_MAJOR}[args.order]
-    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8) | int(os.environ.get("IMCONV_DEBUG_FLAGS", "0"), 0))
+    _lib.lib.imconv_debug_set_flags(args.dbg_flags | (args.rps << 8) | args.host_flags)
     def once():
         if args.explicit:
             low = K.im2col_nhwc(x, sp.h_f, sp.w_f, *sp.conv_args(), True)

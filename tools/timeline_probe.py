@@ -10,7 +10,6 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["IMCONV_INSTRUMENTED"] = "1"
 
 
 def main():
@@ -21,6 +20,7 @@ def main():
     args = ap.parse_args()
     import torch
     from paper_2110_03901_b200 import _lib
+    _lib.use_instrumented()
     from paper_2110_03901_b200._kernels import conv_device
     from paper_2110_03901_b200.workloads import baseline_configs
     layers = {l.name: l for l in baseline_configs()["cfg4"]}
