@@ -88,6 +88,56 @@ def committed_traffic(config: str, world: int):
                                              f"(csrc {d['csrc_sha']}; not measured in this run)")
 
 
+def measure_traffic(args, launches: int, timeout_s: float = 420.0):
+    """DRAM bytes of one step measured in this run: a child process runs the same workload
+    (one pass, eager launches) under `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
+    gpu__time_duration.sum` and the bytes of that pass's `launches` conv kernels are summed
+    (B200_PROFILING.md launch-list recipe).  The child's timings are never reported as a bench
+    value; only its DRAM byte counters are.  Returns (bytes per step or None, note, rows)."""
+    import csv
+    import io
+    import shutil
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu is None:
+        return None, "ncu not found", None
+    log = os.path.join("/tmp", f"imconv_traffic_{os.getpid()}.csv")
+    child = [sys.executable, os.path.abspath(__file__), "--config", args.config, "--traffic-child"]
+    if args.emulate_world > 1:
+        child += ["--emulate-world", str(args.emulate_world)]
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", "regex:conv_", "-s", str(launches), "-c", str(launches),
+           "--csv", "--log-file", log] + child
+    env = dict(os.environ)
+    for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    try:
+        r = subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.PIPE, text=True,
+                           timeout=timeout_s, env=env)
+        if r.returncode != 0:
+            return None, f"ncu child failed (rc {r.returncode}): {r.stderr.strip()[-200:]}", None
+        with open(log) as fh:
+            rows = [row for row in csv.reader(io.StringIO(fh.read())) if len(row) > 10]
+    except Exception as e:  # noqa: BLE001 -- the measurement is optional; say why it is absent
+        return None, f"ncu child failed: {type(e).__name__}: {e}", None
+    finally:
+        if os.path.exists(log):
+            os.remove(log)
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1.0, "usecond": 1e3,
+             "msecond": 1e6}
+    h = rows[0]
+    iid, im, iu, iv, ik = (h.index("ID"), h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value"),
+                           h.index("Kernel Name"))
+    per = {}
+    for row in rows[1:]:
+        d = per.setdefault(row[iid], {"kernel": row[ik].split("(")[0].replace("void ", "")})
+        d[row[im]] = float(row[iv].replace(",", "")) * scale.get(row[iu], 1.0)
+    if len(per) != launches:
+        return None, f"ncu child profiled {len(per)} launches, expected {launches}", None
+    total = sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0) for d in per.values())
+    return total, (f"measured in this run: ncu dram__bytes_read+write summed over the {launches} conv launches "
+                   f"of one eager pass of the same workload in a child process"), list(per.values())
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -418,6 +468,9 @@ def main(argv=None):
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--layers-json", default=None, help="write per-layer timings here (rank 0)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the in-run ncu DRAM-traffic measurement (report the committed figure if any)")
+    ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--emulate-world", type=int, default=0,
                     help="diagnostic (1 process): run rank 0's shard of a W-rank job and report W x its "
                          "throughput, i.e. what the W-GPU run measures when every rank matches rank 0")
@@ -487,6 +540,10 @@ def main(argv=None):
     one_pass(work)
     torch.cuda.synchronize()
     launches_per_pass = int(_lib.lib.imconv_launch_count())
+    if args.traffic_child:  # ncu child of measure_traffic: the profiled pass, then exit
+        one_pass(work)
+        torch.cuda.synchronize()
+        return 0
 
     graph = None
     if not args.no_graph:
@@ -665,7 +722,15 @@ def main(argv=None):
                "sample": f"{args.config}: all {len(layers_full)} layers at batch {n_s} of {layers_full[0].spec.n} "
                          f"({desc}; {secs[0]:.1f} s)"}
 
-    traffic, traffic_note = committed_traffic(args.config, shard_world)
+    traffic, traffic_note, traffic_rows = None, "not measured (--no-traffic)", None
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic, traffic_note, traffic_rows = measure_traffic(args, launches_per_pass)
+    if traffic is None:
+        committed, note = committed_traffic(args.config, shard_world)
+        if committed is not None:
+            traffic, traffic_note = committed, note
+        else:
+            traffic_note += f"; {note}"
     # the stem executes C = 8 (3 image channels zero-padded, as BASELINE.json defines it);
     # the same run with only the 3 useful channels counted
     useful_value = None
@@ -696,6 +761,12 @@ def main(argv=None):
                          "traffic": traffic,
                          "traffic_unit": "DRAM bytes per step per GPU (ncu dram__bytes_read+write)",
                          "traffic_source": traffic_note,
+                         **({"traffic_over_alg": traffic / bytes_alg_rank} if traffic else {}),
+                         **({"ncu_pass_us": sum(d.get("gpu__time_duration.sum", 0.0) for d in traffic_rows) / 1e3,
+                             "ncu_top_launch": max(({"kernel": d["kernel"][:60], "us": d.get("gpu__time_duration.sum", 0.0) / 1e3,
+                                                     "dram_bytes": d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)}
+                                                    for d in traffic_rows), key=lambda e: e["us"])}
+                            if traffic_rows else {}),
                          "bytes_alg": bytes_alg_rank,
                          "peak_kind": peak_name,
                          "kernel": "conv kernels (generic / row-band / halo), all layers of the step",

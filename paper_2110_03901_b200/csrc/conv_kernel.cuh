@@ -121,30 +121,34 @@ struct KWalk {
     }
 };
 
-// Work units of one persistent CTA (round-robin over the grid): whole tiles
-// [0, full_end), then -- split-K tail -- unit v = u - full_end < tail*S is
-// split v % S of tile full_end + v / S over k-stages [kb0, kb1).  Every role
-// walks the same sequence.
+// Work units of one persistent CTA (round-robin over the grid).  Split-K tail
+// (S > 1): the tiles [sk_first, total) are split S ways and their units come
+// FIRST -- unit v < tail*S is split v % S of tile sk_first + v / S over
+// k-stages [kb0, kb1) -- then the whole tiles [0, sk_first) follow.  A split
+// unit is therefore the first unit of its CTA (tail*S <= grid): every split of
+// a tile starts at launch and arrives together, and its partial-sum exchange
+// runs in the epilogue warps while the MMA warp already streams the CTA's next
+// (whole) tile into the other TMEM accumulator.  Every role walks the same sequence.
 struct Unit {
     long long tile;
     int kb0, kb1, split;  // split < 0: the whole tile
 };
-__device__ __forceinline__ bool get_unit(long long u, long long full_end, long long total, int S, int k_stages,
+__device__ __forceinline__ bool get_unit(long long u, long long sk_first, long long total, int S, int k_stages,
                                          Unit &w) {
-    if (u < full_end) {
-        w.tile = u;
-        w.kb0 = 0;
-        w.kb1 = k_stages;
-        w.split = -1;
+    const long long n_split = S > 1 ? (total - sk_first) * S : 0;
+    if (u < n_split) {
+        w.tile = sk_first + u / S;
+        w.split = static_cast<int>(u % S);
+        w.kb0 = w.split * k_stages / S;
+        w.kb1 = (w.split + 1) * k_stages / S;
         return true;
     }
-    if (S <= 1) return false;
-    const long long v = u - full_end;
-    if (v >= (total - full_end) * S) return false;
-    w.tile = full_end + v / S;
-    w.split = static_cast<int>(v % S);
-    w.kb0 = w.split * k_stages / S;
-    w.kb1 = (w.split + 1) * k_stages / S;
+    const long long t = u - n_split;
+    if (t >= (S > 1 ? sk_first : total)) return false;
+    w.tile = t;
+    w.kb0 = 0;
+    w.kb1 = k_stages;
+    w.split = -1;
     return true;
 }
 
@@ -343,8 +347,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     // and all k-subtiles of a block fit the B ring -> the filter slice is loaded
     // once into ring slots 0..k_stages-1 and only A streams (1x1 layers, C*e <= 4*128 B)
     const bool b_res = CG == 1 && KSUB == 1 && p.b_resident && !p.a_gather && k_stages <= STAGES;
-    // split-K tail (host guarantees sk_first is a multiple of the grid)
-    const int S = (CG == 1 && !p.a_gather && !b_res && p.sk_split > 1) ? p.sk_split : 1;
+    // split-K tail: tiles [sk_first, total) split S ways, their units first (get_unit)
+    const int S = (!p.a_gather && !b_res && p.sk_split > 1) ? p.sk_split : 1;
     const long long full_end = S > 1 ? p.sk_first : total_tiles;
 
     if (warp == 0 && lane == 0) {
@@ -881,44 +885,49 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         ptx::mbar_arrive(&tempty[acc]);
                 }
             } else {
-                // ---- split-K unit: raw 32-bit partial sums -> workspace; every split then reduces
-                // the output blocks it owns (block b of the tile: m-tile mt, kOC-column chunk j,
-                // b = mt * (BN / kOC) + j, owned by split b % S) ----
-                // Workspace per tail tile: [split][block][kOC/4 column quads][128 rows][4 words],
-                // so a warp writes 512 contiguous bytes per store and an owner fetches each
-                // peer's block with ONE bulk copy; the reduction reads smem conflict-free.
+                // ---- split-K unit (always its CTA's FIRST unit, see get_unit) ----
+                // The tile's output blocks (block b = mt * (BN / kOC) + j: m-tile mt, kOC-column
+                // chunk j) are owned round-robin by the splits (owner = b % S).  Each split writes
+                // the raw 32-bit partial sums of the blocks it does NOT own to the workspace,
+                // arrives on the tile's ticket counter and waits for the other splits (they all
+                // started at launch); it then adds the peers' partials of its own blocks, in
+                // split order (deterministic sums), to its accumulator -- still in TMEM -- and
+                // stores them.  Meanwhile the MMA warp already runs the CTA's next unit in the
+                // other TMEM accumulator, so the exchange is hidden behind a whole tile.
+                // Workspace per (tail tile, CTA of a pair): [split][block][kOC/4 quads][128 rows]
+                // [4 words]: one warp-wide store / load of a quad covers 512 contiguous bytes.
                 constexpr int kBlocks = MT * (BN / kOC);
                 constexpr uint32_t kBlkWords = kBM * kOC;  // 32 KiB (16-bit out) / 16 KiB (32-bit out)
-                const long long tt = tile - full_end;
-                uint32_t *ws_tile = reinterpret_cast<uint32_t *>(p.sk_ws) + tt * S * (Cfg::kRows * BN);
-                uint32_t *ws_mine = ws_tile + static_cast<long long>(wu.split) * (Cfg::kRows * BN);
+                const long long tt = (tile - full_end) * CG + rank;
+                const uint32_t *ws_tile = reinterpret_cast<const uint32_t *>(p.sk_ws) + tt * S * (Cfg::kRows * BN);
+                uint32_t *ws_mine = const_cast<uint32_t *>(ws_tile) + static_cast<long long>(wu.split) * (Cfg::kRows * BN);
+                const long long rbase = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows;
+                const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                      static_cast<uint32_t>(acc * MT * BN);
                 long long ts[6];
                 ts[0] = IMCONV_INSTRUMENT ? clock64() : 0;
 #pragma unroll 1
                 for (int b = 0; b < kBlocks; ++b) {
                     const int mt = b / (BN / kOC), j = b - mt * (BN / kOC);
-                    if (n_tile * BN + j * kOC >= p.k || m_tile * Cfg::kRows + mt * kBM >= p.m) continue;
+                    if (b % S == wu.split) continue;  // owned: stays in TMEM
+                    if (n_tile * BN + j * kOC >= p.k || rbase + mt * kBM >= p.m) continue;
                     uint32_t v[kOC];
 #pragma unroll
                     for (int h = 0; h < kOC / 32; ++h)
-                        ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                                    static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC + h * 32),
+                        ptx::tmem_ld_32x32b_x32(tacc + static_cast<uint32_t>(mt * BN + j * kOC + h * 32),
                                                 *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
                     ptx::tmem_ld_wait();
                     uint4 *dst = reinterpret_cast<uint4 *>(ws_mine + b * kBlkWords) + row;
 #pragma unroll
                     for (int q = 0; q < kOC / 4; ++q) dst[q * kBM] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                 }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
                 ts[1] = IMCONV_INSTRUMENT ? clock64() : 0;
-                __threadfence();                      // this thread's partial is visible GPU-wide ...
+                __threadfence();                      // this thread's partials are visible GPU-wide ...
                 ptx::named_bar_sync(5, 128);          // ... for all four epilogue warps
                 ts[2] = IMCONV_INSTRUMENT ? clock64() : 0;
                 if (warp == 4 && lane == 0) {
-                    // arrive, then wait for the tile's other splits (all co-resident: the tail
-                    // units are the last unit of distinct persistent CTAs)
+                    // arrive, then wait for the tile's other splits (co-resident: every split is
+                    // the first unit of a distinct persistent CTA, grid <= resident CTAs)
                     unsigned long long *slot = p.sk_cnt + tt;
                     bool last = false;
                     const unsigned long long target = sk_arrive(slot, S, last);
@@ -926,7 +935,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         const long long t0 = clock64();
                         uint32_t tries = 0;
                         while (ptx::ld_acquire_gpu(slot) < target) {
-                            __nanosleep(64);
+                            __nanosleep(32);
                             // a peer that never arrives is a planner bug (non-resident split): fail loudly
                             if ((++tries & 1023u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
                         }
@@ -935,61 +944,52 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                 }
                 ptx::named_bar_sync(6, 160);          // all partials visible -> epilogue warps and the store warp
                 ts[3] = IMCONV_INSTRUMENT ? clock64() : 0;
-                ts[4] = 0;
-                // the operand ring is idle (this tail unit is the CTA's last: its MMAs, hence every
-                // load into the ring, have completed), so it receives the peers' partial blocks
-                const uint32_t ring = ptx::smem_u32(smem_a);
-                constexpr uint32_t kRing = STAGES * (Cfg::kAStageK + Cfg::kBStage);
-                const int per_round = static_cast<int>(kRing / (S * kBlkWords * 4));  // >= 1 (host: S <= 5)
-                uint32_t sk_phase = 0;
-                int b = wu.split;
-                while (b < kBlocks) {
-                    // one round: up to per_round owned blocks, S bulk copies each
-                    int nb = 0, bl[8];
-                    for (int bb = b; bb < kBlocks && nb < per_round && nb < 8; bb += S) {
-                        const int mt = bb / (BN / kOC), j = bb - mt * (BN / kOC);
-                        if (n_tile * BN + j * kOC < p.k && m_tile * Cfg::kRows + mt * kBM < p.m) bl[nb++] = bb;
-                        b = bb + S;
-                    }
-                    if (nb == 0) break;
-                    if (warp == 4 && lane == 0) {
-                        ptx::fence_proxy_async_global();
-                        const uint64_t pol = ptx::policy_evict_first();
-                        ptx::mbar_arrive_expect_tx(sk_bar, static_cast<uint32_t>(nb * S * kBlkWords * 4));
-                        for (int i = 0; i < nb; ++i)
-                            for (int s2 = 0; s2 < S; ++s2)
-                                ptx::bulk_load(ring + (i * S + s2) * (kBlkWords * 4),
-                                               ws_tile + static_cast<long long>(s2) * (Cfg::kRows * BN) + bl[i] * kBlkWords,
-                                               kBlkWords * 4, sk_bar, pol);
-                    }
-                    ptx::mbar_wait(sk_bar, sk_phase);
-                    if (IMCONV_INSTRUMENT && ts[4] == 0) ts[4] = clock64();
-                    sk_phase ^= 1;
-                    for (int i = 0; i < nb; ++i) {
-                        uint32_t v[kOC];
+                ts[4] = ts[3];
+#pragma unroll 1
+                for (int b = wu.split; b < kBlocks; b += S) {
+                    const int mt = b / (BN / kOC), j = b - mt * (BN / kOC);
+                    if (n_tile * BN + j * kOC >= p.k || rbase + mt * kBM >= p.m) continue;
+                    uint32_t v[kOC];
 #pragma unroll
-                        for (int q = 0; q < kOC; ++q) v[q] = 0u;
-                        for (int s2 = 0; s2 < S; ++s2) {  // fixed order: deterministic sums
-                            const uint32_t src = ring + (i * S + s2) * (kBlkWords * 4) + row * 16;
+                    for (int q = 0; q < kOC; ++q) v[q] = 0u;
+                    for (int s2 = 0; s2 < S; ++s2) {  // fixed split order: deterministic sums
+                        uint32_t t[kOC];
+                        if (s2 == wu.split) {
+#pragma unroll
+                            for (int h = 0; h < kOC / 32; ++h)
+                                ptx::tmem_ld_32x32b_x32(tacc + static_cast<uint32_t>(mt * BN + j * kOC + h * 32),
+                                                        *reinterpret_cast<uint32_t(*)[32]>(t + 32 * h));
+                            ptx::tmem_ld_wait();
+                        } else {
+                            const uint4 *src = reinterpret_cast<const uint4 *>(
+                                                   ws_tile + static_cast<long long>(s2) * (Cfg::kRows * BN) + b * kBlkWords) + row;
 #pragma unroll
                             for (int q = 0; q < kOC / 4; ++q) {
-                                uint32_t t[4];
-                                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                             : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3])
-                                             : "r"(src + q * (kBM * 16)));
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    if constexpr (OUT == OUT_I32)
-                                        v[4 * q + e] += t[e];  // int32 two's complement
-                                    else
-                                        v[4 * q + e] = __float_as_uint(__uint_as_float(v[4 * q + e]) +
-                                                                       __uint_as_float(t[e]));
-                                }
+                                const uint4 u4 = ptx::ld_global_cg_v4(src + q * kBM);
+                                t[4 * q] = u4.x;
+                                t[4 * q + 1] = u4.y;
+                                t[4 * q + 2] = u4.z;
+                                t[4 * q + 3] = u4.w;
                             }
                         }
-                        stage_chunk(v);
+#pragma unroll
+                        for (int e = 0; e < kOC; ++e) {
+                            if constexpr (OUT == OUT_I32)
+                                v[e] += t[e];  // int32 two's complement
+                            else
+                                v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(t[e]));
+                        }
                     }
-                    ptx::named_bar_sync(5, 128);  // every thread has read this round's blocks
+                    stage_chunk(v);
+                }
+                // every TMEM load of this accumulator has completed: release it
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2)
+                        ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+                    else
+                        ptx::mbar_arrive(&tempty[acc]);
                 }
                 if (IMCONV_INSTRUMENT && p.dbg && warp == 4 && lane == 0) {
                     ts[5] = clock64();

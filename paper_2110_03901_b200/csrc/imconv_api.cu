@@ -42,6 +42,7 @@ constexpr int kDbgNoStemSpec = 1 << 23;   // row-band kernel: no compile-time st
 constexpr int kDbgNoHaloStack = 1 << 25;  // halo kernel: one sub-block per block (no shared N = 128 taps)
 constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep the generic kernel
 constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-stationary layout
+constexpr int kDbgNoPairSplit = 1 << 28;  // CTA pairs never split the tail wave's k-loops
 
 // Split-K ticket counters (conv_kernel.cuh sk_arrive): one per tail tile, never
 // cleared (they only grow, in steps that leave a multiple of kSkRound between
@@ -868,32 +869,39 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
     g->sk_tail = 0;
     // Splits of one tile spin-wait for each other, so every CTA of the grid must be
     // resident at once: never with a caller grid above one CTA per SM.
-    if (!cl && !g->use_pair && !a_gather && !g->b_resident && grid <= sms && !(g_debug_flags & kDbgNoSplitK)) {
+    // CTA pairs split pair tiles over clusters (g0 = grid / 2 pairs; a pair's two CTAs exchange
+    // their own 128-row halves with the same-rank CTAs of the other splits).
+    if (!cl && !a_gather && !g->b_resident && grid <= sms && !(g_debug_flags & kDbgNoSplitK) &&
+        !(g->use_pair && (g_debug_flags & kDbgNoPairSplit))) {
         const int k_st = (g->k_subs + g->ksub - 1) / g->ksub;
-        const long long g0 = grid;
+        const long long g0 = g->use_pair ? grid / 2 : grid;
         const long long tail = g->tiles >= g0 ? g->tiles % g0 : g->tiles;
         // Measured (tools/small_n_probe.py): the partials' L2 round trip (write 4 B per
-        // output, fence, peer wait, bulk read back) costs ~5-7k cycles per split, so only
-        // long k-loops gain (3x3 with C >= 256: 36+ stages); 16-32-stage 1x1 layers lose.
-        constexpr int kSkMaxSplit = 5, kSkMinStages = 36;
+        // output, fence, peer wait, read back) costs ~5-7k cycles per split.  Below one wave
+        // it is exposed, so only long k-loops gain (3x3 with C >= 256: 36+ stages).  Behind
+        // full waves the split units run first and the exchange hides behind the CTA's next
+        // whole tile (get_unit): k-loops of >= 24 stages gain (tools/ab_layers.py: s5 3x3 at
+        // N = 256 49.6 -> 41.1 us, s5 1x1a (32 stages) 26.0 -> 23.9; 16-stage 1x1 layers lose ~8%).
+        constexpr int kSkMaxSplit = 5, kSkMinStages = 36, kSkMinStagesHidden = 24;
         const bool sub_wave = g->tiles < g0 && k_st >= kSkMinStages;
-        const bool short_tail = tail > 0 && 2 * tail <= g0 && g->tiles < 2 * g0 && k_st >= kSkMinStages;
+        const bool short_tail = g->tiles >= g0 && tail > 0 && 2 * tail <= g0 && k_st >= kSkMinStagesHidden;
         if (sub_wave || short_tail) {
             const int Sk = static_cast<int>(std::min<long long>(
                 {g0 / tail, static_cast<long long>(k_st / 4), kSkMaxSplit}));
-            // and only when the stages saved (k_st * (1 - 1/S) at ~600 cycles) beat the
-            // ~15k-cycle partial round trip: a 3-way split of a 36-stage tail loses
-            // (s4 3x3 at N = 128: 31.6 us split vs 29.3 us with CTA pairs)
-            if (Sk >= 2 && tail <= kSkSliceLen &&
-                static_cast<long long>(k_st) * (Sk - 1) > static_cast<long long>(kSkCyclesPerSplit / 600) * Sk) {
+            // sub-wave: only when the stages saved (k_st * (1 - 1/S) at ~600 cycles) beat the
+            // ~15k-cycle exposed round trip (a 3-way split of a 36-stage k-loop loses: s4 3x3
+            // at N = 128, 31.6 us split vs 29.3 us with CTA pairs)
+            const bool pays = short_tail || static_cast<long long>(k_st) * (Sk - 1) >
+                                                static_cast<long long>(kSkCyclesPerSplit / 600) * Sk;
+            if (Sk >= 2 && tail * (g->use_pair ? 2 : 1) <= kSkSliceLen && pays) {
                 g->sk_split = Sk;
                 g->sk_tail = tail;
-                if (g->tiles < g0) grid = static_cast<int>(tail * Sk);
+                if (g->tiles < g0) grid = static_cast<int>(tail * Sk * (g->use_pair ? 2 : 1));
             }
         }
     }
     if (g->use_pair) {
-        if (grid > 2 * g->tiles) grid = static_cast<int>(2 * g->tiles);
+        if (g->sk_split == 1 && grid > 2 * g->tiles) grid = static_cast<int>(2 * g->tiles);
         if (grid < 2) grid = 2;
     } else if (g->sk_split == 1 && grid > g->tiles) {
         grid = static_cast<int>(g->tiles);
@@ -937,8 +945,10 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
         // half of B) cut the per-SM operand bytes per stage by a third and run a 6-deep
         // ring.  Measured N = 256: s4 1x1a 29.4 -> 26.6 us, s4 proj 51.7 -> 46.3,
         // s5 1x1b 25.7 -> 23.9, s4 3x3 42.2 -> 40.7; B-stationary and split-K layers lose.
-        if (!g->b_resident && g->sk_split == 1 && !(a->flags & IMCONV_FLAG_SINGLE_CTA) &&
-            !(g_debug_flags & kDbgNoAutoPair)) {
+        // With >= 2 waves the pair's per-stage saving outweighs a single-CTA split tail (s5
+        // 1x1a / proj at N = 256: pair 43.3 / 40.4 us, 128 x 256 + split tail 48.1 / 44.8).
+        // A pair plan may carry its own split tail (pair tiles over grid / 2 clusters).
+        if (!g->b_resident && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && !(g_debug_flags & kDbgNoAutoPair)) {
             GenericPlan h;
             if (plan_generic_bn(a, P, Q, sms, 256, -1, &h, true) == 0 && h.use_pair) *g = h;
         }
@@ -1087,22 +1097,21 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
             }
         }
     };
-    // persistent round-robin; split-K tail units as in get_unit (conv_kernel.cuh)
+    // persistent round-robin; split-K tail units first, as in get_unit (conv_kernel.cuh)
     const long long G = g.use_pair ? g.grid / 2 : g.grid;
-    const long long full_end = g.sk_split > 1 ? g.tiles - g.sk_tail : g.tiles;
+    const long long sk_first = g.sk_split > 1 ? g.tiles - g.sk_tail : g.tiles;
+    const long long n_split = g.sk_split > 1 ? g.sk_tail * g.sk_split : 0;
     const int k_stages = (g.k_subs + g.ksub - 1) / g.ksub;
     struct U { long long tile; int kb0, kb1; bool last_split; };
     auto unit = [&](long long ui, U &u) {
-        if (ui < full_end) {
-            u = {ui, 0, k_stages, true};
+        if (ui < n_split) {
+            const int sp = static_cast<int>(ui % g.sk_split);
+            u = {sk_first + ui / g.sk_split, sp * k_stages / g.sk_split, (sp + 1) * k_stages / g.sk_split,
+                 sp == g.sk_split - 1};
             return true;
         }
-        if (g.sk_split <= 1) return false;
-        const long long v = ui - full_end;
-        if (v >= g.sk_tail * g.sk_split) return false;
-        const int sp = static_cast<int>(v % g.sk_split);
-        u = {full_end + v / g.sk_split, sp * k_stages / g.sk_split, (sp + 1) * k_stages / g.sk_split,
-             sp == g.sk_split - 1};
+        if (ui - n_split >= sk_first) return false;
+        u = {ui - n_split, 0, k_stages, true};
         return true;
     };
     std::vector<uint8_t> b_loaded(static_cast<size_t>(G), 0);
@@ -1428,28 +1437,17 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = plan.grid;
     p.b_resident = plan.b_resident ? 1 : 0;
-    if (use_pair) {
-        const int g2 = grid;
-        switch (a->in_dtype) {
-            case IMCONV_BF16:
-                return a->out_dtype == IMCONV_F32 ? dispatch_bn_pair<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
-                                                  : dispatch_bn_pair<ELEM_BF16, OUT_BF16>(bn, ta, tb, ty, p, g2, st);
-            case IMCONV_F16:
-                return a->out_dtype == IMCONV_F32 ? dispatch_bn_pair<ELEM_F16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
-                                                  : dispatch_bn_pair<ELEM_F16, OUT_F16>(bn, ta, tb, ty, p, g2, st);
-            case IMCONV_I8: return dispatch_bn_pair<ELEM_I8, OUT_I32>(bn, ta, tb, ty, p, g2, st);
-            default: return IMCONV_EDTYPE;
-        }
-    }
 
-    // split-K tail (plan_generic): stream-ordered partial-sum workspace + tagged counters
+    // split-K tail (plan_generic): stream-ordered partial-sum workspace + ticket counters
     void *sk_ws = nullptr;
     p.sk_split = 1;
     if (plan.sk_split > 1) {
         int dev = 0;
         cudaGetDevice(&dev);
         unsigned long long *cnt = sk_counters(dev);
-        const size_t ws_bytes = static_cast<size_t>(plan.sk_tail) * plan.sk_split * (kBM * mt) * bn * 4;
+        const int cg = use_pair ? 2 : 1;
+        const size_t ws_bytes = static_cast<size_t>(plan.sk_tail) * plan.sk_split * cg * (kBM * mt) * bn * 4;
+        if (plan.sk_tail * cg > kSkSliceLen) return IMCONV_EINVAL;  // (planner guarantees it)
         if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
             const unsigned long long slice = g_sk_slice.fetch_add(1) % kSkSlices;
             p.sk_split = plan.sk_split;
@@ -1459,8 +1457,26 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         } else {
             sk_ws = nullptr;
             cudaGetLastError();  // (allocation failure: run without splitting)
-            grid = static_cast<int>(std::min<long long>(grid, tiles));
+            grid = static_cast<int>(std::min<long long>(grid, tiles * cg));
         }
+    }
+    if (use_pair) {
+        const int g2 = grid;
+        int rc_pair;
+        switch (a->in_dtype) {
+            case IMCONV_BF16:
+                rc_pair = a->out_dtype == IMCONV_F32 ? dispatch_bn_pair<ELEM_BF16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
+                                                     : dispatch_bn_pair<ELEM_BF16, OUT_BF16>(bn, ta, tb, ty, p, g2, st);
+                break;
+            case IMCONV_F16:
+                rc_pair = a->out_dtype == IMCONV_F32 ? dispatch_bn_pair<ELEM_F16, OUT_F32>(bn, ta, tb, ty, p, g2, st)
+                                                     : dispatch_bn_pair<ELEM_F16, OUT_F16>(bn, ta, tb, ty, p, g2, st);
+                break;
+            case IMCONV_I8: rc_pair = dispatch_bn_pair<ELEM_I8, OUT_I32>(bn, ta, tb, ty, p, g2, st); break;
+            default: rc_pair = IMCONV_EDTYPE;
+        }
+        if (sk_ws) cudaFreeAsync(sk_ws, st);
+        return rc_pair;
     }
     int rc_launch;
     switch (a->in_dtype) {

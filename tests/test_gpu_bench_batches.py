@@ -44,9 +44,9 @@ def _operands(layer, sp, seed, dev):
 
 # branches each shard size must exercise (imconv_plan labels; see the module docstring)
 EXPECTED_BRANCHES = {
-    256: {"row-band", "halo", "halo-stream", "generic 256x256 pair", "generic 128x256 split3",
+    256: {"row-band", "halo", "halo-stream", "generic 256x256 pair", "generic 256x256 pair split3",
           "generic 128x256 b-stationary", "generic 256x64 b-stationary"},
-    128: {"row-band", "halo", "generic 256x128", "generic 256x256 pair", "generic 128x256"},
+    128: {"row-band", "halo", "generic 256x128", "generic 256x256 pair", "generic 256x256 pair split3", "generic 128x256"},
     64: {"halo-stream", "generic 128x256", "generic 128x128 ksub2", "generic 256x256 pair"},
     32: {"halo-stream", "generic 128x256 split5", "generic 128x128 ksub2", "generic 256x256 pair"},
 }
@@ -83,7 +83,7 @@ def test_resnet50_shapes_at_shard_batch(n):
 def _tail_first_image(pl, sp):
     """First image whose output rows belong to a split-K tail block."""
     first_tile = pl.tiles - pl.sk_tail
-    rows_per_block = 128 * pl.mt
+    rows_per_block = 128 * pl.mt * (2 if pl.cta_pair else 1)
     n_tiles = -(-sp.c_o // pl.bn)
     return int((first_tile // n_tiles) * rows_per_block // (sp.h_o * sp.w_o))
 
@@ -91,8 +91,8 @@ def _tail_first_image(pl, sp):
 def test_split_k_graph_replay_bit_exact():
     """Split-K tails captured in ONE CUDA graph and replayed 300 times, the inputs rewritten
     before every replay: every replay's output is bit-exact.  Cases: s5 3x3 at 256 images
-    (3-way split, bf16 out), s5 3x3 at 32 images (5-way, fp32 out), an int8 5-way split
-    (C = K = 1024 at 16 images).
+    (CTA pairs, 3-way split, bf16 out), s5 3x3 at 32 images (5-way, fp32 out), an int8 5-way
+    split (C = K = 1024 at 16 images) and an int8 CTA-pair 2-way split (128 images).
     Integer-valued operands scaled by a per-replay factor c: y(c x) = c y(x) exactly, so a
     split that reads a peer's stale partial (an earlier replay's) or skips the wait fails."""
     import paper_2110_03901_b200 as P
@@ -107,6 +107,8 @@ def test_split_k_graph_replay_bit_exact():
         (ConvSpec.square(32, 512, 7, 512, 3, stride=1, pad=1), torch.bfloat16, torch.float32, 5),
         # int8: s5 3x3 at 32 images plans 128 x 128 blocks with no split; C = K = 1024 at 16 splits 5 ways
         (ConvSpec.square(16, 1024, 7, 1024, 3, stride=1, pad=1), torch.int8, torch.int32, 5),
+        # CTA pairs with a split tail (pair tiles over 74 clusters), int8
+        (ConvSpec.square(128, 1024, 7, 1024, 3, stride=1, pad=1), torch.int8, torch.int32, 2),
     ]
     work = []
     for sp, cdt, odt, want_split in cases:
