@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define IMCONV_ABI_VERSION 3
+#define IMCONV_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define IMCONV_API __attribute__((visibility("default")))
@@ -219,7 +219,8 @@ typedef struct imconv_plan_info {
     int32_t b_resident;  /* 1: each CTA loads its filter slice once */
     int32_t sk_split;    /* split-K ways of the tail tiles (1 = no split) */
     int64_t tiles;       /* output blocks */
-    int64_t sk_tail;     /* tail blocks whose k-loop is split */
+    int64_t sk_tail;     /* tail blocks whose k-loop is split (sk_mode 1) or streamed (sk_mode 2) */
+    int32_t sk_mode;     /* 0 whole blocks, 1 split-K tail, 2 stream-K over the last two waves */
 } imconv_plan_info;
 IMCONV_API int imconv_plan(const imconv_conv_args *args, int32_t sms, imconv_plan_info *out);
 

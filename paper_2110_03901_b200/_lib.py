@@ -70,6 +70,7 @@ class ImconvPlanInfo(ctypes.Structure):
         ("kernel", ctypes.c_int32), ("grid", ctypes.c_int32), ("bn", ctypes.c_int32), ("mt", ctypes.c_int32),
         ("ksub", ctypes.c_int32), ("cta_pair", ctypes.c_int32), ("b_resident", ctypes.c_int32),
         ("sk_split", ctypes.c_int32), ("tiles", ctypes.c_int64), ("sk_tail", ctypes.c_int64),
+        ("sk_mode", ctypes.c_int32),
     ]
 
 

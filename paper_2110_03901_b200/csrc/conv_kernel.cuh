@@ -73,8 +73,9 @@ struct ConvParams {
     int b_3d;            // 1: the filter map is 3-D {chunk cols, rows, chunks}: one TMA per stage for all of B
     int a_gather;        // 1: 16-byte pixels -- A tap blocks gathered by cp.async warps instead of TMA
     const uint8_t *x;    // NHWC input (gather mode)
-    int sk_split;        // split-K tail: S > 1 splits each of the last (total - sk_first) tiles' k-loop S ways
-    long long sk_first;  // first tail tile (a multiple of the grid: the full waves end here)
+    int sk_mode;         // 0 whole tiles, 1 split-K tail, 2 stream-K (UnitWalk)
+    int sk_split;        // mode 1: S > 1 splits each of the last (total - sk_first) tiles' k-loop S ways
+    long long sk_first;  // modes 1 / 2: first tile of the split / streamed tail
     float *sk_ws;        // fp32 partials [tail tile][S][MT*128 rows][BN]
     unsigned long long *sk_cnt;  // per tail tile ticket counters (monotonic, see sk_arrive)
     int b_resident;      // 1: grid is a multiple of n_tiles (each CTA keeps one output-channel block) --
@@ -121,36 +122,94 @@ struct KWalk {
     }
 };
 
-// Work units of one persistent CTA (round-robin over the grid).  Split-K tail
-// (S > 1): the tiles [sk_first, total) are split S ways and their units come
-// FIRST -- unit v < tail*S is split v % S of tile sk_first + v / S over
-// k-stages [kb0, kb1) -- then the whole tiles [0, sk_first) follow.  A split
-// unit is therefore the first unit of its CTA (tail*S <= grid): every split of
-// a tile starts at launch and arrives together, and its partial-sum exchange
-// runs in the epilogue warps while the MMA warp already streams the CTA's next
-// (whole) tile into the other TMEM accumulator.  Every role walks the same sequence.
+// Work units of one persistent CTA (or CTA pair): every role walks the same
+// sequence, unit ul = 0, 1, 2, ... of CTA c out of G.
+//
+// mode 0: whole tiles round-robin: tile c + ul * G.
+// mode 1 (split-K tail, last wave at most half full): the tiles [sk_first, total)
+//   are split S ways and their units come FIRST -- global unit v = c + ul * G <
+//   tail*S is split v % S of tile sk_first + v / S over k-stages [kb0, kb1) --
+//   then the whole tiles [0, sk_first).  A split unit is therefore the first
+//   unit of its CTA (tail*S <= G): the splits of a tile start at launch and
+//   arrive together, and their partial-sum exchange runs in the epilogue warps
+//   while the MMA warp already streams the CTA's next tile into the other TMEM
+//   accumulator.
+// mode 2 (stream-K, last wave more than half full): the last partial wave plus
+//   one full wave, tiles [sk_first, total), are one stream of
+//   W = (total - sk_first) * k_stages k-stages cut into G equal contiguous
+//   ranges, CTA c taking [c*W/G, (c+1)*W/G) FIRST, then the whole tiles
+//   c + j*G < sk_first.  A range is at least one tile long, so a tile is cut at
+//   most once: its k-end piece starts some CTA's range (the "writer": partial
+//   sums -> workspace, early) and its k-start piece ends the previous CTA's
+//   range (the "finisher": adds the writer's partial to its own and stores,
+//   while the MMA warp runs the CTA's whole tiles).
 struct Unit {
     long long tile;
-    int kb0, kb1, split;  // split < 0: the whole tile
+    int kb0, kb1, split;  // split < 0: the whole tile (or a stream-K piece)
+    int sk;               // stream-K piece: 0 none, 1 writer (k-end piece), 2 finisher (k-start piece)
 };
-__device__ __forceinline__ bool get_unit(long long u, long long sk_first, long long total, int S, int k_stages,
-                                         Unit &w) {
-    const long long n_split = S > 1 ? (total - sk_first) * S : 0;
-    if (u < n_split) {
-        w.tile = sk_first + u / S;
-        w.split = static_cast<int>(u % S);
-        w.kb0 = w.split * k_stages / S;
-        w.kb1 = (w.split + 1) * k_stages / S;
+struct UnitWalk {
+    long long c, G, total, sk_first;
+    int mode, S, k_stages;
+    long long lo, hi;  // mode 2: this CTA's stream range
+    __host__ __device__ __forceinline__ UnitWalk(long long c_, long long G_, long long total_, int mode_, int S_,
+                                                  long long sk_first_, int k_stages_)
+        : c(c_), G(G_), total(total_), sk_first(sk_first_), mode(mode_), S(S_), k_stages(k_stages_), lo(0), hi(0) {
+        if (mode == 2) {
+            const long long W = (total - sk_first) * k_stages;
+            lo = c * W / G;
+            hi = (c + 1) * W / G;
+        }
+    }
+    __host__ __device__ __forceinline__ bool get(long long ul, Unit &w) const {
+        w.sk = 0;
+        w.split = -1;
+        if (mode == 1) {
+            const long long u = c + ul * G;
+            const long long n_split = (total - sk_first) * S;
+            if (u < n_split) {
+                w.tile = sk_first + u / S;
+                w.split = static_cast<int>(u % S);
+                w.kb0 = w.split * k_stages / S;
+                w.kb1 = (w.split + 1) * k_stages / S;
+                return true;
+            }
+            const long long t = u - n_split;
+            if (t >= sk_first) return false;
+            w.tile = t;
+            w.kb0 = 0;
+            w.kb1 = k_stages;
+            return true;
+        }
+        if (mode == 2) {
+            // segments of [lo, hi): the first starts at lo, later ones at tile boundaries
+            const long long first_tile = lo / k_stages;
+            const long long start = ul == 0 ? lo : (first_tile + ul) * k_stages;
+            if (start < hi) {
+                const long long t = start / k_stages;
+                const long long end = hi < (t + 1) * k_stages ? hi : (t + 1) * k_stages;
+                w.tile = sk_first + t;
+                w.kb0 = static_cast<int>(start - t * k_stages);
+                w.kb1 = static_cast<int>(end - t * k_stages);
+                w.sk = (w.kb0 > 0) ? 1 : (w.kb1 < k_stages ? 2 : 0);
+                return true;
+            }
+            const long long n_seg = (hi - 1) / k_stages - first_tile + 1;  // (hi > lo: ranges >= one tile)
+            const long long t = c + (ul - n_seg) * G;
+            if (t >= sk_first) return false;
+            w.tile = t;
+            w.kb0 = 0;
+            w.kb1 = k_stages;
+            return true;
+        }
+        const long long t = c + ul * G;
+        if (t >= total) return false;
+        w.tile = t;
+        w.kb0 = 0;
+        w.kb1 = k_stages;
         return true;
     }
-    const long long t = u - n_split;
-    if (t >= (S > 1 ? sk_first : total)) return false;
-    w.tile = t;
-    w.kb0 = 0;
-    w.kb1 = k_stages;
-    w.split = -1;
-    return true;
-}
+};
 
 // Arrival of one split on its tail tile's ticket counter.  Counters only grow:
 // between launches a slot holds a multiple of kSkRound; inside a launch each of
@@ -347,9 +406,11 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     // and all k-subtiles of a block fit the B ring -> the filter slice is loaded
     // once into ring slots 0..k_stages-1 and only A streams (1x1 layers, C*e <= 4*128 B)
     const bool b_res = CG == 1 && KSUB == 1 && p.b_resident && !p.a_gather && k_stages <= STAGES;
-    // split-K tail: tiles [sk_first, total) split S ways, their units first (get_unit)
-    const int S = (!p.a_gather && !b_res && p.sk_split > 1) ? p.sk_split : 1;
-    const long long full_end = S > 1 ? p.sk_first : total_tiles;
+    // split-K tail (mode 1) / stream-K (mode 2) over the tiles [sk_first, total) (UnitWalk)
+    const int sk_mode = (!p.a_gather && !b_res) ? p.sk_mode : 0;
+    const int S = sk_mode == 1 ? p.sk_split : 1;
+    const long long full_end = sk_mode ? p.sk_first : total_tiles;
+    const UnitWalk walk(tile_start, tile_step, total_tiles, sk_mode, S, full_end, k_stages);
 
     if (warp == 0 && lane == 0) {
 #if IMCONV_INSTRUMENT
@@ -596,7 +657,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             const long long t_start = clock64();
             KWalk kw;
             Unit wu;
-            for (long long ui = tile_start; get_unit(ui, full_end, total_tiles, S, k_stages, wu); ui += tile_step) {
+            for (long long ul = 0; walk.get(ul, wu); ++ul) {
                 const long long tile = wu.tile;
                 const long long m_tile = tile / p.n_tiles;
                 const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
@@ -753,13 +814,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         if (b_res) ptx::mbar_wait(bres, 0);
         const long long t_start = clock64();
         Unit wu;
-        for (long long ui = tile_start; get_unit(ui, full_end, total_tiles, S, k_stages, wu); ui += tile_step) {
+        for (long long ul = 0; walk.get(ul, wu); ++ul) {
             timed_wait_g(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
             const uint32_t d_base = tmem_u + static_cast<uint32_t>(acc * MT * BN);
             for (int kb = wu.kb0; kb < wu.kb1; ++kb) {
                 timed_wait_g(&full[stage], phase, w_full);
-                if (IMCONV_INSTRUMENT && ui == tile_start && kb == wu.kb0 && lane == 0) tl_stamp(p.dbg, tl_idx, 2);
+                if (IMCONV_INSTRUMENT && ul == 0 && kb == wu.kb0 && lane == 0) tl_stamp(p.dbg, tl_idx, 2);
                 ptx::tc_fence_after();
                 {
                     // descriptors as (low, high) words: only the start-address field moves
@@ -844,14 +905,42 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             ++chunk_ctr;
         };
         Unit wu;
-        for (long long ui = tile_start; get_unit(ui, full_end, total_tiles, S, k_stages, wu); ui += tile_step) {
+        for (long long ul = 0; walk.get(ul, wu); ++ul) {
             const long long tile = wu.tile;
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
             timed_wait_g(&tfull[acc], acc_phase, w_tfull);
-            if (IMCONV_INSTRUMENT && ui == tile_start && warp == 4 && lane == 0) tl_stamp(p.dbg, tl_idx, 4);
+            if (IMCONV_INSTRUMENT && ul == 0 && warp == 4 && lane == 0) tl_stamp(p.dbg, tl_idx, 4);
             ptx::tc_fence_after();
             if (wu.split < 0) {
+                // stream-K pieces (UnitWalk mode 2): the writer (k-end piece) parks its partial sums
+                // in the tile's workspace slot ([block][kOC/4 quads][128 rows][4 words] per CTA of a
+                // pair); the finisher (k-start piece, later in its CTA's range) waits for it and adds
+                // it to its own accumulator (fixed order: finisher + writer, deterministic).
+                constexpr uint32_t kBlkWords = kBM * kOC;
+                uint32_t *ws_sk = nullptr;
+                unsigned long long *sk_slot = nullptr;
+                if (wu.sk) {
+                    const long long tt = (tile - full_end) * CG + rank;
+                    ws_sk = reinterpret_cast<uint32_t *>(p.sk_ws) + tt * (Cfg::kRows * BN);
+                    sk_slot = p.sk_cnt + tt;
+                }
+                if (wu.sk == 2) {
+                    if (warp == 4 && lane == 0) {
+                        bool last = false;
+                        const unsigned long long target = sk_arrive(sk_slot, 2, last);
+                        if (!last) {
+                            const long long t0 = clock64();
+                            uint32_t tries = 0;
+                            while (ptx::ld_acquire_gpu(sk_slot) < target) {
+                                __nanosleep(32);
+                                if ((++tries & 1023u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
+                            }
+                        }
+                        __threadfence();
+                    }
+                    ptx::named_bar_sync(5, 128);  // the writer's partial is visible to all epilogue warps
+                }
 #pragma unroll 1
                 for (int mt = 0; mt < MT; ++mt) {
                     const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;
@@ -868,11 +957,42 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                             ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
                         ptx::tmem_ld_wait();
                         const long long e1 = IMCONV_INSTRUMENT ? clock64() : 0;
+                        if (wu.sk == 1) {
+                            uint4 *dst = reinterpret_cast<uint4 *>(ws_sk + (mt * (BN / kOC) + j) * kBlkWords) + row;
+#pragma unroll
+                            for (int q = 0; q < kOC / 4; ++q)
+                                dst[q * kBM] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                            continue;
+                        }
+                        if (wu.sk == 2) {
+                            const uint4 *src =
+                                reinterpret_cast<const uint4 *>(ws_sk + (mt * (BN / kOC) + j) * kBlkWords) + row;
+#pragma unroll
+                            for (int q = 0; q < kOC / 4; ++q) {
+                                const uint4 u4 = ptx::ld_global_cg_v4(src + q * kBM);
+                                const uint32_t t[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    if constexpr (OUT == OUT_I32)
+                                        v[4 * q + e] += t[e];
+                                    else
+                                        v[4 * q + e] = __float_as_uint(__uint_as_float(v[4 * q + e]) + __uint_as_float(t[e]));
+                                }
+                            }
+                        }
                         stage_chunk(v);
                         if (IMCONV_INSTRUMENT) {
                             t_ld += e1 - e0;
                             t_st += clock64() - e1;
                         }
+                    }
+                }
+                if (wu.sk == 1) {
+                    __threadfence();              // this thread's partials are visible GPU-wide ...
+                    ptx::named_bar_sync(5, 128);  // ... for all four epilogue warps: publish
+                    if (warp == 4 && lane == 0) {
+                        bool last = false;
+                        sk_arrive(sk_slot, 2, last);  // the writer never waits
                     }
                 }
                 // every TMEM load of this accumulator has completed: release it
@@ -1016,11 +1136,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         constexpr int kOC = Cfg::kOutCols;
         uint32_t chunk_ctr = 0;
         Unit wu;
-        for (long long ui = tile_start; get_unit(ui, full_end, total_tiles, S, k_stages, wu); ui += tile_step) {
+        for (long long ul = 0; walk.get(ul, wu); ++ul) {
             const long long tile = wu.tile;
             const long long m_tile = tile / p.n_tiles;
             const int n_tile = static_cast<int>(tile - m_tile * p.n_tiles);
-            // split-K unit: this split stores the blocks it owns (b % S == split)
+            // split-K unit: this split stores the blocks it owns (b % S == split);
+            // a stream-K writer piece stores nothing (its finisher does)
+            if (wu.sk == 1) continue;
             if (wu.split >= 0) ptx::named_bar_sync(6, 160);
             for (int mt = 0; mt < MT; ++mt) {
                 const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;

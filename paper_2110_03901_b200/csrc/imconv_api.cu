@@ -43,6 +43,7 @@ constexpr int kDbgNoHaloStack = 1 << 25;  // halo kernel: one sub-block per bloc
 constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep the generic kernel
 constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-stationary layout
 constexpr int kDbgNoPairSplit = 1 << 28;  // CTA pairs never split the tail wave's k-loops
+constexpr int kDbgStreamK = 1 << 29;      // stream-K the last two waves (measured slower: opt-in, see below)
 
 // Split-K ticket counters (conv_kernel.cuh sk_arrive): one per tail tile, never
 // cleared (they only grow, in steps that leave a multiple of kSkRound between
@@ -780,13 +781,15 @@ struct GenericPlan {
     int grid;
     bool b_resident;
     int sk_split;        // 1 = off
-    long long sk_tail;   // tail tiles split S ways (sk_split > 1)
+    long long sk_tail;   // sk_mode 1: tail tiles split S ways; sk_mode 2: tiles of the stream-K region
+    int sk_mode;         // 0 whole tiles, 1 split-K tail, 2 stream-K (conv_kernel.cuh UnitWalk)
 };
 
 // One candidate block shape: bn output channels, variant_force >= 0 overrides
 // the m-tile / k-subtile variant (see dispatch_bn).
 // split-K: cycles one split tail pays for the partials' L2 round trip (fitted, see plan_generic)
 constexpr int kSkCyclesPerSplit = 15000;
+constexpr int kSkStreamMinStages = 8;  // stream-K: shortest k-loop (stages) worth cutting
 
 int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, int bn_req, int variant_force,
                     GenericPlan *g, bool pair_force = false) {
@@ -867,6 +870,7 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
     // keeps >= 4 pipeline stages; S <= 5 so S peer blocks fit the idle operand ring.
     g->sk_split = 1;
     g->sk_tail = 0;
+    g->sk_mode = 0;
     // Splits of one tile spin-wait for each other, so every CTA of the grid must be
     // resident at once: never with a caller grid above one CTA per SM.
     // CTA pairs split pair tiles over clusters (g0 = grid / 2 pairs; a pair's two CTAs exchange
@@ -896,8 +900,22 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
             if (Sk >= 2 && tail * (g->use_pair ? 2 : 1) <= kSkSliceLen && pays) {
                 g->sk_split = Sk;
                 g->sk_tail = tail;
+                g->sk_mode = 1;
                 if (g->tiles < g0) grid = static_cast<int>(tail * Sk * (g->use_pair ? 2 : 1));
             }
+        }
+        // Stream-K (opt-in, kDbgStreamK): a last wave more than half full cannot be split S >= 2
+        // ways, so the last partial wave and one full wave are streamed as equal k-ranges over all
+        // CTAs (a tile is cut at most once; the writer/finisher exchange runs in the epilogue).
+        // Measured slower on every candidate (tools/ab_layers.py, N = 256: s4 3x3 41.1 -> 43.6 us,
+        // s4 1x1a 27.4 -> 39.1; N = 128 s5 1x1b 15.3 -> 26.6): every cut tile moves a 128 KB fp32
+        // partial per CTA through L2 twice, and the epilogue's global-store throughput (~32 GB/s
+        // per SM, the same limit as the output stream) makes that cost more than the wave saved.
+        const long long n_sk = tail + g0;
+        if (g->sk_mode == 0 && g->tiles >= g0 && 2 * tail > g0 && tail < g0 && k_st >= kSkStreamMinStages &&
+            n_sk * (g->use_pair ? 2 : 1) <= kSkSliceLen && (g_debug_flags & kDbgStreamK)) {
+            g->sk_mode = 2;
+            g->sk_tail = n_sk;
         }
     }
     if (g->use_pair) {
@@ -965,9 +983,9 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
     // 128 x 256 + 3-way split 16.3).
     auto cost = [&](const GenericPlan &q, double cyc_stage) {
         const double k_st = static_cast<double>((q.k_subs + q.ksub - 1) / q.ksub);
-        const long long full = q.tiles - q.sk_tail;
+        const long long full = q.tiles - (q.sk_mode == 1 ? q.sk_tail : 0);
         const long long full_waves = (full + q.grid - 1) / q.grid;
-        const long long tail_waves = q.sk_split > 1 ? (q.sk_tail * q.sk_split + q.grid - 1) / q.grid : 0;
+        const long long tail_waves = q.sk_mode == 1 ? (q.sk_tail * q.sk_split + q.grid - 1) / q.grid : 0;
         return static_cast<double>(full_waves) * k_st * cyc_stage +
                static_cast<double>(tail_waves) * (k_st / q.sk_split * cyc_stage + kSkCyclesPerSplit);
     };
@@ -1097,21 +1115,20 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
             }
         }
     };
-    // persistent round-robin; split-K tail units first, as in get_unit (conv_kernel.cuh)
+    // persistent schedule: the kernel's own unit walk (conv_kernel.cuh UnitWalk)
     const long long G = g.use_pair ? g.grid / 2 : g.grid;
-    const long long sk_first = g.sk_split > 1 ? g.tiles - g.sk_tail : g.tiles;
-    const long long n_split = g.sk_split > 1 ? g.sk_tail * g.sk_split : 0;
+    const long long sk_first = g.sk_mode ? g.tiles - g.sk_tail : g.tiles;
     const int k_stages = (g.k_subs + g.ksub - 1) / g.ksub;
-    struct U { long long tile; int kb0, kb1; bool last_split; };
-    auto unit = [&](long long ui, U &u) {
-        if (ui < n_split) {
-            const int sp = static_cast<int>(ui % g.sk_split);
-            u = {sk_first + ui / g.sk_split, sp * k_stages / g.sk_split, (sp + 1) * k_stages / g.sk_split,
-                 sp == g.sk_split - 1};
-            return true;
-        }
-        if (ui - n_split >= sk_first) return false;
-        u = {ui - n_split, 0, k_stages, true};
+    struct U { long long tile; int kb0, kb1; bool stores; };
+    // round r of CTA b = its r-th unit (rounds advance together in the replay)
+    auto unit = [&](long long b, long long round, U &u) {
+        const UnitWalk wk(b, G, g.tiles, g.sk_mode, g.sk_split, sk_first, k_stages);
+        Unit w;
+        if (!wk.get(round, w)) return false;
+        // the output lines are written by the split that stores them (the last split, as an
+        // approximation of the owner spread) or by a stream-K finisher / whole tile
+        const bool stores = g.sk_mode == 1 ? (w.split < 0 || w.split == g.sk_split - 1) : w.sk != 1;
+        u = {w.tile, w.kb0, w.kb1, stores};
         return true;
     };
     std::vector<uint8_t> b_loaded(static_cast<size_t>(G), 0);
@@ -1120,7 +1137,7 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
         for (int kb = 0; kb < k_stages; ++kb) {
             for (long long b = 0; b < G; ++b) {
                 U u;
-                if (!unit(b + round * G, u) || kb < u.kb0 || kb >= u.kb1) continue;
+                if (!unit(b, round, u) || kb < u.kb0 || kb >= u.kb1) continue;
                 any = true;
                 const long long m_tile = u.tile / g.n_tiles;
                 const int n_tile = static_cast<int>(u.tile - m_tile * g.n_tiles);
@@ -1132,7 +1149,7 @@ int predict_traffic_impl(const imconv_conv_args *a, int64_t l2_bytes, int sms, i
                 }
                 if (kb == u.kb1 - 1) {
                     if (g.b_resident) b_loaded[static_cast<size_t>(b)] = 1;
-                    if (u.last_split) y_lines(m_tile, n_tile);
+                    if (u.stores) y_lines(m_tile, n_tile);
                 }
             }
         }
@@ -1243,6 +1260,7 @@ extern "C" int imconv_plan(const imconv_conv_args *a, int32_t sms, imconv_plan_i
     out->sk_split = g.sk_split;
     out->tiles = g.tiles;
     out->sk_tail = g.sk_tail;
+    out->sk_mode = g.sk_mode;
     return 0;
 }
 
@@ -1441,15 +1459,19 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     // split-K tail (plan_generic): stream-ordered partial-sum workspace + ticket counters
     void *sk_ws = nullptr;
     p.sk_split = 1;
-    if (plan.sk_split > 1) {
+    p.sk_mode = 0;
+    if (plan.sk_mode) {
         int dev = 0;
         cudaGetDevice(&dev);
         unsigned long long *cnt = sk_counters(dev);
         const int cg = use_pair ? 2 : 1;
-        const size_t ws_bytes = static_cast<size_t>(plan.sk_tail) * plan.sk_split * cg * (kBM * mt) * bn * 4;
+        // mode 1: S partials per tail tile; mode 2: one (the writer's) per streamed tile
+        const size_t ws_bytes = static_cast<size_t>(plan.sk_tail) * (plan.sk_mode == 1 ? plan.sk_split : 1) * cg *
+                                (kBM * mt) * bn * 4;
         if (plan.sk_tail * cg > kSkSliceLen) return IMCONV_EINVAL;  // (planner guarantees it)
         if (cnt && cudaMallocAsync(&sk_ws, ws_bytes, st) == cudaSuccess) {
             const unsigned long long slice = g_sk_slice.fetch_add(1) % kSkSlices;
+            p.sk_mode = plan.sk_mode;
             p.sk_split = plan.sk_split;
             p.sk_first = tiles - plan.sk_tail;
             p.sk_ws = static_cast<float *>(sk_ws);

@@ -54,6 +54,7 @@ class LaunchPlan:
     sk_split: int
     tiles: int
     sk_tail: int
+    sk_mode: int = 0
 
     @property
     def branch(self) -> str:
@@ -67,6 +68,8 @@ class LaunchPlan:
             parts.append("b-stationary")
         if self.sk_split > 1:
             parts.append(f"split{self.sk_split}")
+        if self.sk_mode == 2:
+            parts.append("stream-k")
         if self.ksub > 1:
             parts.append(f"ksub{self.ksub}")
         return "generic " + " ".join(parts)
@@ -97,7 +100,7 @@ def plan(spec: ConvSpec, dtype: str = "bf16", sms: int = 148, out_dtype: str | N
     t = _lib.ImconvPlanInfo()
     _lib.check(_lib.lib.imconv_plan(ctypes.byref(a), int(sms), ctypes.byref(t)), "imconv_plan")
     return LaunchPlan(KERNELS.get(t.kernel, "?"), t.grid, t.bn, t.mt, t.ksub, bool(t.cta_pair), bool(t.b_resident),
-                      t.sk_split, t.tiles, t.sk_tail)
+                      t.sk_split, t.tiles, t.sk_tail, t.sk_mode)
 
 
 def predict(spec: ConvSpec, dtype: str = "bf16", order: str = "reuse_aware", l2_bytes: int = L2_BYTES_B200,

@@ -45,6 +45,7 @@ def _operands(layer, sp, seed, dev):
 # branches each shard size must exercise (imconv_plan labels; see the module docstring)
 EXPECTED_BRANCHES = {
     256: {"row-band", "halo", "halo-stream", "generic 256x256 pair", "generic 256x256 pair split3",
+
           "generic 128x256 b-stationary", "generic 256x64 b-stationary"},
     128: {"row-band", "halo", "generic 256x128", "generic 256x256 pair", "generic 256x256 pair split3", "generic 128x256"},
     64: {"halo-stream", "generic 128x256", "generic 128x128 ksub2", "generic 256x256 pair"},
@@ -102,18 +103,24 @@ def test_split_k_graph_replay_bit_exact():
     from paper_2110_03901_b200.traffic import plan
     dev = torch.device("cuda", 0)
     rng = np.random.default_rng(11)
-    cases = [  # (spec, compute dtype, out dtype, expected split)
-        (ConvSpec.square(256, 512, 7, 512, 3, stride=1, pad=1), torch.bfloat16, torch.bfloat16, 3),
-        (ConvSpec.square(32, 512, 7, 512, 3, stride=1, pad=1), torch.bfloat16, torch.float32, 5),
+    cases = [  # (spec, compute dtype, out dtype, expected split, expected sk_mode)
+        (ConvSpec.square(256, 512, 7, 512, 3, stride=1, pad=1), torch.bfloat16, torch.bfloat16, 3, 1),
+        (ConvSpec.square(32, 512, 7, 512, 3, stride=1, pad=1), torch.bfloat16, torch.float32, 5, 1),
         # int8: s5 3x3 at 32 images plans 128 x 128 blocks with no split; C = K = 1024 at 16 splits 5 ways
-        (ConvSpec.square(16, 1024, 7, 1024, 3, stride=1, pad=1), torch.int8, torch.int32, 5),
+        (ConvSpec.square(16, 1024, 7, 1024, 3, stride=1, pad=1), torch.int8, torch.int32, 5, 1),
         # CTA pairs with a split tail (pair tiles over 74 clusters), int8
-        (ConvSpec.square(128, 1024, 7, 1024, 3, stride=1, pad=1), torch.int8, torch.int32, 2),
+        (ConvSpec.square(128, 1024, 7, 1024, 3, stride=1, pad=1), torch.int8, torch.int32, 2, 1),
+        # stream-K over the last two waves (opt-in planner switch, set during capture below):
+        # s4 3x3 at 256 images (CTA pairs), s3 3x3 at 128 (single CTAs)
+        (ConvSpec.square(256, 256, 14, 256, 3, stride=1, pad=1), torch.bfloat16, torch.bfloat16, 1, 2),
+        (ConvSpec.square(128, 128, 28, 128, 3, stride=1, pad=1), torch.bfloat16, torch.float32, 1, 2),
     ]
+    STREAM_K = 1 << 29  # imconv_api.cu kDbgStreamK
+    P._lib.lib.imconv_debug_set_flags(STREAM_K)
     work = []
-    for sp, cdt, odt, want_split in cases:
-        pl = plan(sp, dtype="int8" if cdt == torch.int8 else "bf16")
-        assert pl.kernel == "generic" and pl.sk_split == want_split, (sp, pl)
+    for sp, cdt, odt, want_split, want_mode in cases:
+        pl = plan(sp, dtype="int8" if cdt == torch.int8 else "bf16", flags=P._lib.FLAG_STATIC_FILTER)
+        assert pl.kernel == "generic" and pl.sk_split == want_split and pl.sk_mode == want_mode, (sp, pl)
         lim = 42 if cdt == torch.int8 else 2  # |c * x| <= 126 (int8, |c| <= 3) / 6 (exact in bf16)
         bases = [rng.integers(-lim, lim + 1, size=(sp.n, sp.h_i, sp.w_i, sp.c_i)) for _ in range(2)]
         w = rng.integers(-lim, lim + 1, size=(sp.h_f, sp.w_f, sp.c_i, sp.c_o))
@@ -139,6 +146,7 @@ def test_split_k_graph_replay_bit_exact():
     with torch.cuda.graph(g, stream=s):
         for sp, x, xs, wd, y, *_ in work:
             conv_device(x, wd, *sp.conv_args(), y=y, out_dtype=y.dtype, flags=P._lib.FLAG_STATIC_FILTER)
+    P._lib.lib.imconv_debug_set_flags(0)
     factors = [1, -2, 3, -1, 2, -3]
     for it in range(300):
         c = factors[it % len(factors)]

@@ -21,7 +21,8 @@ def main():
     ap.add_argument("--a", type=lambda v: int(v, 0), default=0)
     ap.add_argument("--b", type=lambda v: int(v, 0), default=0x80000)
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--unique", action="store_true", help="--layers all: every unique cfg4 shape")
+    ap.add_argument("--data", default="int", choices=["int", "randn"],
+                    help="int: integer-valued (outputs compared); randn: bench.py-like N(0,1) / Kaiming")
     args = ap.parse_args()
     import torch
     import paper_2110_03901_b200 as P
@@ -74,8 +75,13 @@ def main():
         for name in names:
             sp = by[name].spec
             g = torch.Generator(device=dev).manual_seed(5)
-            x = torch.randint(-2, 3, (sp.n, sp.h_i, sp.w_i, sp.c_i), generator=g, device=dev).to(torch.bfloat16)
-            w = torch.randint(-2, 3, (sp.h_f, sp.w_f, sp.c_i, sp.c_o), generator=g, device=dev).to(torch.bfloat16)
+            if args.data == "int":
+                x = torch.randint(-2, 3, (sp.n, sp.h_i, sp.w_i, sp.c_i), generator=g, device=dev).to(torch.bfloat16)
+                w = torch.randint(-2, 3, (sp.h_f, sp.w_f, sp.c_i, sp.c_o), generator=g, device=dev).to(torch.bfloat16)
+            else:
+                x = torch.randn((sp.n, sp.h_i, sp.w_i, sp.c_i), generator=g, device=dev).to(torch.bfloat16)
+                w = (torch.randn((sp.h_f, sp.w_f, sp.c_i, sp.c_o), generator=g, device=dev)
+                     * (2.0 / (sp.c_i * sp.h_f * sp.w_f)) ** 0.5).to(torch.bfloat16)
             ya = torch.empty((sp.n, sp.h_o, sp.w_o, sp.c_o), device=dev, dtype=torch.bfloat16)
             yb = torch.empty_like(ya)
             _lib.lib.imconv_debug_set_flags(args.a)
@@ -91,7 +97,7 @@ def main():
                 tb.append(best(gb))
             same = torch.equal(ya, yb)
             print(f"| {name} | {n} | {pa} | {pb} | {min(ta):.2f} | {min(tb):.2f} | {min(tb) / min(ta):.3f} | "
-                  f"{'identical' if same else 'DIFFER'} |", flush=True)
+                  f"{'identical' if same else ('DIFFER' if args.data == 'int' else 'differ (float sums)')} |", flush=True)
             del ga, gb, x, w, ya, yb
 
 
