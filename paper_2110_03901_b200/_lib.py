@@ -17,6 +17,9 @@ LIB_PATH = os.path.join(_PKG, "libimconv.so")
 # the same sources built with per-role wait counters (-DIMCONV_INSTRUMENT=1): loaded only
 # by diagnostic tools that ask for it explicitly (use_instrumented), never by the package
 LIB_INSTR_PATH = os.path.join(_PKG, "libimconv_instr.so")
+# the same sources with the device / planner invariant checks on (-DIMCONV_DEBUG=1): loaded
+# only by tests/debug_check.py (use_debug), never by the package
+LIB_DEBUG_PATH = os.path.join(_PKG, "libimconv_debug.so")
 _loaded = None
 
 # element-type codes, include/imconv.h
@@ -122,14 +125,25 @@ def _load(path: str):
     return L
 
 
+def _use(path: str) -> None:
+    global _loaded
+    if _loaded is not None and _loaded[0] != path:
+        raise RuntimeError(f"{_loaded[0]} is already loaded in this process")
+    _loaded = (path, _load(path))
+    globals()["lib"] = _loaded[1]
+
+
 def use_instrumented() -> None:
     """Diagnostics only (tools/run_layer.py --waits, tools/timeline_probe.py): bind the
     instrumented build instead of the product library.  Must precede any other use."""
-    global _loaded
-    if _loaded is not None and _loaded[0] != LIB_INSTR_PATH:
-        raise RuntimeError("libimconv.so is already loaded in this process")
-    _loaded = (LIB_INSTR_PATH, _load(LIB_INSTR_PATH))
-    globals()["lib"] = _loaded[1]
+    _use(LIB_INSTR_PATH)
+
+
+def use_debug() -> None:
+    """Checks only (tests/debug_check.py): bind the debug-invariant build (device asserts on
+    mbarrier phases, TMEM allocation, split-K tickets, work units, staged/stored chunk counts;
+    host asserts on the planner's schedule).  Must precede any other use."""
+    _use(LIB_DEBUG_PATH)
 
 
 def __getattr__(name):

@@ -19,6 +19,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libimconv.so")
 LIB_INSTR = os.path.join(PKG, "libimconv_instr.so")  # same sources, -DIMCONV_INSTRUMENT=1 (tools only)
+LIB_DEBUG = os.path.join(PKG, "libimconv_debug.so")  # same sources, -DIMCONV_DEBUG=1: invariant checks
 SOURCES = [os.path.join(CSRC, f) for f in ("imconv_api.cu", "lru.cpp")]
 # every header the sources can include: a stale .so must never survive an edit to one of them
 HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) + [
@@ -37,13 +38,15 @@ def _stale(lib: str) -> bool:
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False, instrument: bool = False) -> str:
-    lib = LIB_INSTR if instrument else LIB
+def build(force: bool = False, verbose: bool = False, instrument: bool = False, debug: bool = False) -> str:
+    lib = LIB_INSTR if instrument else LIB_DEBUG if debug else LIB
     if not force and not _stale(lib):
         return lib
     cmd = [NVCC] + ARCH + FLAGS + ["-I", os.path.join(ROOT, "include"), "-shared", "-o", lib] + SOURCES
     if instrument:
         cmd.insert(1, "-DIMCONV_INSTRUMENT=1")
+    if debug:
+        cmd.insert(1, "-DIMCONV_DEBUG=1")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
@@ -52,4 +55,5 @@ def build(force: bool = False, verbose: bool = False, instrument: bool = False) 
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="-v" in sys.argv, instrument="--instrument" in sys.argv))
+    print(build(force=True, verbose="-v" in sys.argv, instrument="--instrument" in sys.argv,
+                debug="--debug" in sys.argv))

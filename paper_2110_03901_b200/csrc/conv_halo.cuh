@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    IMCONV_CHECK((tmem_base >> 16) == 0 && (tmem_base & 0xffffu) + (Cfg::kTmemCols) <= 512u,
+                 "TMEM allocation outside the 512 columns", tmem_base, (Cfg::kTmemCols));
     // PDL: setup above overlaps the previous kernel's tail; no global memory is
     // touched before every prerequisite grid has completed
     ptx::griddep_launch_dependents();

@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    IMCONV_CHECK((tmem_base >> 16) == 0 && (tmem_base & 0xffffu) + (Cfg::kTmemCols) <= 512u,
+                 "TMEM allocation outside the 512 columns", tmem_base, (Cfg::kTmemCols));
     // PDL: setup above overlaps the previous kernel's tail
     ptx::griddep_launch_dependents();
     if (!(p.b_early && warp == 3)) ptx::griddep_wait();

@@ -223,6 +223,8 @@ constexpr unsigned long long kSkRound = 64;
 __device__ __forceinline__ unsigned long long sk_arrive(unsigned long long *slot, int S, bool &last) {
     const unsigned long long old = atomicAdd(slot, 1ull);
     const unsigned long long base = old & ~(kSkRound - 1);
+    IMCONV_CHECK(old - base < static_cast<unsigned long long>(S), "split-K ticket: more arrivals than splits in a round",
+                 old, S);
     last = old - base == static_cast<unsigned long long>(S - 1);
     if (last) atomicAdd(slot, kSkRound - static_cast<unsigned long long>(S));
     return base + static_cast<unsigned long long>(S);
@@ -450,7 +452,10 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    IMCONV_CHECK((tmem_base >> 16) == 0 && (tmem_base & 0xffffu) + Cfg::kTmemCols <= 512u,
+                 "TMEM allocation outside the 512 columns", tmem_base, Cfg::kTmemCols);
     const uint32_t tl_idx = IMCONV_INSTRUMENT ? *tl_slot : 0u;
+    volatile uint32_t *dbg_chunks = tmem_slot + 4;  // debug builds: staged / stored chunk counts
     // PDL: setup above overlaps the previous kernel's tail; no global memory is
     // touched before every prerequisite grid has completed
     ptx::griddep_launch_dependents();
@@ -815,6 +820,8 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         const long long t_start = clock64();
         Unit wu;
         for (long long ul = 0; walk.get(ul, wu); ++ul) {
+            IMCONV_CHECK(wu.kb0 < wu.kb1 && wu.kb1 <= k_stages && wu.tile >= 0 && wu.tile < total_tiles,
+                         "work unit outside the tile / k-stage space", wu.tile, wu.kb0 * 65536 + wu.kb1);
             timed_wait_g(&tempty[acc], acc_phase ^ 1, w_tempty);
             ptx::tc_fence_after();
             const uint32_t d_base = tmem_u + static_cast<uint32_t>(acc * MT * BN);
@@ -1124,6 +1131,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         // the store warp frees the second-to-last tile after the last chunk: consume
         // that arrival so no named barrier is left half-arrived at exit
         if (chunk_ctr >= 2) ptx::named_bar_sync(3 + (chunk_ctr & 1), 160);
+        if (IMCONV_DEBUG && warp == 4 && lane == 0) dbg_chunks[0] = chunk_ctr;
         if (IMCONV_INSTRUMENT && p.dbg && lane == 0 && quarter == 0) {
             p.dbg[blockIdx.x * 8 + 5] = clock64() - t_start;
             p.dbg[blockIdx.x * 8 + 6] = w_tfull;
@@ -1167,6 +1175,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
         // only the staging reads must finish before exit: the grid's completion (what a
         // dependent launch waits on) covers the global writes still in flight
         if (lane == 0) ptx::tma_store_wait_read<0>();
+        if (IMCONV_DEBUG && lane == 0) dbg_chunks[1] = chunk_ctr;
         if (IMCONV_INSTRUMENT && lane == 0) tl_stamp(p.dbg, tl_idx, 5);
         __syncwarp();
     }
@@ -1185,6 +1194,10 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
         }
     }
+    // every chunk the epilogue staged was stored exactly once (debug builds)
+    if (IMCONV_DEBUG && threadIdx.x == 0)
+        IMCONV_CHECK(dbg_chunks[0] == dbg_chunks[1], "epilogue staged / store warp stored chunk counts differ",
+                     dbg_chunks[0], dbg_chunks[1]);
     if (IMCONV_INSTRUMENT && threadIdx.x == 0) tl_stamp(p.dbg, tl_idx, 6);
 }
 

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -1291,6 +1292,26 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
     GenericPlan plan;
     rc = plan_generic(a, P, Q, sms, &plan);
     if (rc) return rc;
+#if IMCONV_DEBUG
+    // debug builds: the planner's schedule invariants (what the kernels' waits rely on)
+    {
+        const long long G = plan.use_pair ? plan.grid / 2 : plan.grid;
+        const char *bad = nullptr;
+        if (plan.grid > sms) bad = "grid above one CTA per SM";
+        else if (plan.use_pair && (plan.grid & 1)) bad = "odd grid for CTA pairs";
+        else if (plan.sk_mode == 1 && (plan.sk_split < 2 || plan.sk_tail * plan.sk_split > G))
+            bad = "split-K units exceed the co-resident CTAs";
+        else if (plan.sk_mode == 2 && (plan.sk_tail < G || plan.sk_tail > plan.tiles))
+            bad = "stream-K region shorter than one tile per CTA";
+        else if (plan.sk_mode && plan.sk_tail * (plan.use_pair ? 2 : 1) > kSkSliceLen)
+            bad = "split-K counters exceed one slice";
+        if (bad) {
+            std::fprintf(stderr, "imconv debug: planner invariant violated: %s (grid %d, tiles %lld, mode %d, S %d, tail %lld)\n",
+                         bad, plan.grid, plan.tiles, plan.sk_mode, plan.sk_split, plan.sk_tail);
+            return IMCONV_EINVAL;
+        }
+    }
+#endif
     const int bn = plan.bn, variant = plan.variant, mt = plan.mt;
     const bool use_pair = plan.use_pair;
 

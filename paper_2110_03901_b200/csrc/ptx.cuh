@@ -8,6 +8,30 @@
 #ifndef IMCONV_INSTRUMENT
 #define IMCONV_INSTRUMENT 0
 #endif
+// Debug-invariant build (libimconv_debug.so, -DIMCONV_DEBUG=1): the pipeline
+// invariants below are checked on the device and a violation prints what broke
+// and traps (the host sees cudaErrorLaunchFailure).  It stands in for
+// compute-sanitizer, which this pool does not offer.  Production builds compile
+// every check away.
+#ifndef IMCONV_DEBUG
+#define IMCONV_DEBUG 0
+#endif
+#include <cstdio>
+#if IMCONV_DEBUG
+#define IMCONV_CHECK(cond, what, a, b)                                                                     \
+    do {                                                                                                  \
+        if (!(cond)) {                                                                                    \
+            printf("imconv invariant violated: %s (block %d thread %d: %lld, %lld)\n", what,            \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x), static_cast<long long>(a), \
+                   static_cast<long long>(b));                                                           \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define IMCONV_CHECK(cond, what, a, b) \
+    do {                               \
+    } while (0)
+#endif
 
 namespace imconv {
 namespace ptx {
@@ -73,13 +97,18 @@ __device__ __forceinline__ bool mbar_test_wait(uint32_t addr, uint32_t parity) {
 // NANOSLEEP loop that wakes late).  A watchdog turns a pipeline deadlock into
 // a trap -- an error the host sees -- instead of a hung GPU: after ~2^34
 // cycles (~9 s) of waiting on one phase, far beyond any legitimate wait.
+// Debug builds: a ~1 s watchdog that names the barrier (shared-memory offset) and phase.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     if (mbar_try_wait(addr, parity)) return;
     const long long t0 = clock64();
     uint32_t tries = 0;
+    constexpr long long kLimit = IMCONV_DEBUG ? (1ll << 31) : (1ll << 34);
     while (!mbar_try_wait(addr, parity)) {
-        if ((++tries & 1023u) == 0 && clock64() - t0 > (1ll << 34)) __trap();
+        if ((++tries & 1023u) == 0 && clock64() - t0 > kLimit) {
+            IMCONV_CHECK(false, "mbarrier phase never completed (smem offset, parity)", addr, parity);
+            __trap();
+        }
     }
 }
 

@@ -167,3 +167,18 @@ def test_split_k_graph_replay_bit_exact():
         yy = conv_device(x, wd, *sp.conv_args(), out_dtype=odt)
         ref = exp[1] if odt != torch.bfloat16 else exp[1].float().bfloat16().to(torch.float64)
         assert torch.equal(yy.index_select(0, idx).to(torch.float64), ref)
+
+
+def test_debug_invariant_build():
+    """Every kernel path through the debug-invariant build (libimconv_debug.so): device checks
+    on mbarrier phases, TMEM allocation, split-K / stream-K tickets, work units and epilogue
+    chunk counts, host checks on the planner's schedule; outputs bit-exact on integer data.
+    Runs in its own process (the debug library is bound explicitly, never by the package)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "debug_check.py")], capture_output=True,
+                       text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "all cases clean and exact" in r.stdout
