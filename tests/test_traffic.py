@@ -113,8 +113,10 @@ def test_launch_plan_branches_of_the_benchmarked_batches():
     assert by_name[256]["s2b0_3x3"].kernel == "halo"
     assert by_name[256]["s3b1_3x3"].kernel == "halo-stream"
     s5 = by_name[256]["s5b0_3x3"]
-    assert s5.kernel == "generic" and s5.sk_split == 3 and s5.sk_tail == 196 % 148
-    assert by_name[256]["s4b0_3x3"].cta_pair
+    # CTA pairs: 98 pair blocks on 74 clusters, the last 24 split 3 ways
+    assert s5.kernel == "generic" and s5.cta_pair and s5.sk_mode == 1 and s5.sk_split == 3
+    assert s5.sk_tail == 98 % 74
+    assert by_name[256]["s4b0_3x3"].cta_pair and by_name[256]["s4b0_3x3"].sk_mode == 0  # stream-K is opt-in
     assert by_name[32]["s5b0_3x3"].sk_split == 5
     # a caller grid above one CTA per SM turns split-K off (splits must be co-resident)
     from paper_2110_03901_b200 import _lib
