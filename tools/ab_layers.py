@@ -19,8 +19,10 @@ def main():
     ap.add_argument("--layers", default="s5b0_3x3")
     ap.add_argument("--n", default="256")
     ap.add_argument("--a", type=lambda v: int(v, 0), default=0)
-    ap.add_argument("--b", type=lambda v: int(v, 0), default=0x80000)
+    ap.add_argument("--b", type=lambda v: int(v, 0), default=0)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--fa", type=lambda v: int(v, 0), default=0, help="imconv flags of arm A (block-shape overrides)")
+    ap.add_argument("--fb", type=lambda v: int(v, 0), default=0, help="imconv flags of arm B")
     ap.add_argument("--data", default="int", choices=["int", "randn"],
                     help="int: integer-valued (outputs compared); randn: bench.py-like N(0,1) / Kaiming")
     args = ap.parse_args()
@@ -33,17 +35,17 @@ def main():
     torch.cuda.set_device(0)
     flags = _lib.FLAG_STATIC_FILTER
 
-    def timed(x, w, y, sp, host):
+    def timed(x, w, y, sp, host, cflags):
         _lib.lib.imconv_debug_set_flags(host)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            conv_device(x, w, *sp.conv_args(), y=y, flags=flags)
+            conv_device(x, w, *sp.conv_args(), y=y, flags=flags | cflags)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             for _ in range(args.reps):
-                conv_device(x, w, *sp.conv_args(), y=y, flags=flags)
+                conv_device(x, w, *sp.conv_args(), y=y, flags=flags | cflags)
         _lib.lib.imconv_debug_set_flags(0)
         g.replay()
         torch.cuda.synchronize()
@@ -85,12 +87,12 @@ def main():
             ya = torch.empty((sp.n, sp.h_o, sp.w_o, sp.c_o), device=dev, dtype=torch.bfloat16)
             yb = torch.empty_like(ya)
             _lib.lib.imconv_debug_set_flags(args.a)
-            pa = plan(sp).branch
+            pa = plan(sp, flags=flags | args.fa).branch
             _lib.lib.imconv_debug_set_flags(args.b)
-            pb = plan(sp).branch
+            pb = plan(sp, flags=flags | args.fb).branch
             _lib.lib.imconv_debug_set_flags(0)
-            ga = timed(x, w, ya, sp, args.a)
-            gb = timed(x, w, yb, sp, args.b)
+            ga = timed(x, w, ya, sp, args.a, args.fa)
+            gb = timed(x, w, yb, sp, args.b, args.fb)
             ta, tb = [], []
             for _ in range(3):
                 ta.append(best(ga))
