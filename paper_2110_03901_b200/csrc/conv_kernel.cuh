@@ -919,19 +919,51 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
             timed_wait_g(&tfull[acc], acc_phase, w_tfull);
             if (IMCONV_INSTRUMENT && ul == 0 && warp == 4 && lane == 0) tl_stamp(p.dbg, tl_idx, 4);
             ptx::tc_fence_after();
-            if (wu.split < 0) {
-                // stream-K pieces (UnitWalk mode 2): the writer (k-end piece) parks its partial sums
-                // in the tile's workspace slot ([block][kOC/4 quads][128 rows][4 words] per CTA of a
-                // pair); the finisher (k-start piece, later in its CTA's range) waits for it and adds
-                // it to its own accumulator (fixed order: finisher + writer, deterministic).
-                constexpr uint32_t kBlkWords = kBM * kOC;
-                uint32_t *ws_sk = nullptr;
-                unsigned long long *sk_slot = nullptr;
-                if (wu.sk) {
-                    const long long tt = (tile - full_end) * CG + rank;
-                    ws_sk = reinterpret_cast<uint32_t *>(p.sk_ws) + tt * (Cfg::kRows * BN);
-                    sk_slot = p.sk_cnt + tt;
+            if (wu.split < 0 && wu.sk == 0) {
+                // ---- whole tile: TMEM -> staged 128 x 128-byte chunks -> the store warp ----
+#pragma unroll 1
+                for (int mt = 0; mt < MT; ++mt) {
+                    const long long row0 = m_tile * (CG * Cfg::kRows) + rank * Cfg::kRows + mt * kBM;
+#pragma unroll 1
+                    for (int j = 0; j < BN / kOC; ++j) {
+                        const int col0 = n_tile * BN + j * kOC;
+                        if (col0 >= p.k || row0 >= p.m) continue;  // uniform (the store warp skips it too)
+                        uint32_t v[kOC];
+                        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                               static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC);
+                        const long long e0 = IMCONV_INSTRUMENT ? clock64() : 0;
+#pragma unroll
+                        for (int h = 0; h < kOC / 32; ++h)
+                            ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
+                        ptx::tmem_ld_wait();
+                        const long long e1 = IMCONV_INSTRUMENT ? clock64() : 0;
+                        stage_chunk(v);
+                        if (IMCONV_INSTRUMENT) {
+                            t_ld += e1 - e0;
+                            t_st += clock64() - e1;
+                        }
+                    }
                 }
+                // every TMEM load of this accumulator has completed: release it
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2)
+                        ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+                    else
+                        ptx::mbar_arrive(&tempty[acc]);
+                }
+            } else if (wu.split < 0) {
+                // ---- stream-K piece (UnitWalk mode 2; kept out of the whole-tile loop above, whose
+                // code generation the output-heavy layers are sensitive to) ----
+                // The writer (k-end piece) parks its partial sums in the tile's workspace slot
+                // ([block][kOC/4 quads][128 rows][4 words] per CTA of a pair); the finisher (k-start
+                // piece, later in its CTA's range) waits for it and adds it to its own accumulator
+                // (fixed order: finisher + writer, deterministic).
+                constexpr uint32_t kBlkWords = kBM * kOC;
+                const long long tt = (tile - full_end) * CG + rank;
+                uint32_t *ws_sk = reinterpret_cast<uint32_t *>(p.sk_ws) + tt * (Cfg::kRows * BN);
+                unsigned long long *sk_slot = p.sk_cnt + tt;
                 if (wu.sk == 2) {
                     if (warp == 4 && lane == 0) {
                         bool last = false;
@@ -958,40 +990,30 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         uint32_t v[kOC];
                         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                                static_cast<uint32_t>(acc * MT * BN + mt * BN + j * kOC);
-                        const long long e0 = IMCONV_INSTRUMENT ? clock64() : 0;
 #pragma unroll
                         for (int h = 0; h < kOC / 32; ++h)
                             ptx::tmem_ld_32x32b_x32(taddr + h * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * h));
                         ptx::tmem_ld_wait();
-                        const long long e1 = IMCONV_INSTRUMENT ? clock64() : 0;
+                        uint4 *blk = reinterpret_cast<uint4 *>(ws_sk + (mt * (BN / kOC) + j) * kBlkWords) + row;
                         if (wu.sk == 1) {
-                            uint4 *dst = reinterpret_cast<uint4 *>(ws_sk + (mt * (BN / kOC) + j) * kBlkWords) + row;
 #pragma unroll
                             for (int q = 0; q < kOC / 4; ++q)
-                                dst[q * kBM] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                                blk[q * kBM] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                             continue;
                         }
-                        if (wu.sk == 2) {
-                            const uint4 *src =
-                                reinterpret_cast<const uint4 *>(ws_sk + (mt * (BN / kOC) + j) * kBlkWords) + row;
 #pragma unroll
-                            for (int q = 0; q < kOC / 4; ++q) {
-                                const uint4 u4 = ptx::ld_global_cg_v4(src + q * kBM);
-                                const uint32_t t[4] = {u4.x, u4.y, u4.z, u4.w};
+                        for (int q = 0; q < kOC / 4; ++q) {
+                            const uint4 u4 = ptx::ld_global_cg_v4(blk + q * kBM);
+                            const uint32_t t[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    if constexpr (OUT == OUT_I32)
-                                        v[4 * q + e] += t[e];
-                                    else
-                                        v[4 * q + e] = __float_as_uint(__uint_as_float(v[4 * q + e]) + __uint_as_float(t[e]));
-                                }
+                            for (int e = 0; e < 4; ++e) {
+                                if constexpr (OUT == OUT_I32)
+                                    v[4 * q + e] += t[e];
+                                else
+                                    v[4 * q + e] = __float_as_uint(__uint_as_float(v[4 * q + e]) + __uint_as_float(t[e]));
                             }
                         }
                         stage_chunk(v);
-                        if (IMCONV_INSTRUMENT) {
-                            t_ld += e1 - e0;
-                            t_st += clock64() - e1;
-                        }
                     }
                 }
                 if (wu.sk == 1) {
@@ -1002,7 +1024,6 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         sk_arrive(sk_slot, 2, last);  // the writer never waits
                     }
                 }
-                // every TMEM load of this accumulator has completed: release it
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
