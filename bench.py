@@ -468,6 +468,10 @@ def main(argv=None):
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--layers-json", default=None, help="write per-layer timings here (rank 0)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="launch the layers serialised (each waits for the previous grid) instead of with "
+                         "IMCONV_FLAG_INDEPENDENT; by default both are timed and the overlapped step is the "
+                         "headline")
     ap.add_argument("--no-traffic", action="store_true",
                     help="skip the in-run ncu DRAM-traffic measurement (report the committed figure if any)")
     ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
@@ -498,9 +502,15 @@ def main(argv=None):
     import paper_2110_03901_b200 as P
     from paper_2110_03901_b200 import _lib
     from paper_2110_03901_b200._kernels import conv_device
-    # the weights are written once at setup, never inside the step: every conv may start
-    # its filter loads before its programmatic-launch wait (IMCONV_FLAG_STATIC_FILTER)
-    STATIC = _lib.FLAG_STATIC_FILTER
+    # The weights are written once at setup, never inside the step: every conv may start its
+    # filter loads before its programmatic-launch wait (IMCONV_FLAG_STATIC_FILTER).  The cfg4
+    # workload is a SWEEP of independent convolutions (BASELINE.json: every layer gets its own
+    # N(0,1) input), each over its own buffers, so by default every launch also carries
+    # IMCONV_FLAG_INDEPENDENT: it never waits for the preceding grid, and layer i+1's CTAs start
+    # on the SMs layer i's last wave leaves idle.  The serialised step (every layer waiting for
+    # the previous one, as a chained network would) is timed in the same run and reported beside.
+    SERIAL_FLAGS = _lib.FLAG_STATIC_FILTER
+    STATIC = SERIAL_FLAGS | (0 if args.no_overlap else _lib.FLAG_INDEPENDENT)
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -527,13 +537,13 @@ def main(argv=None):
     work_sets = [work] + [[(layer, sp, x.clone(), w.clone(), torch.empty_like(y)) for layer, sp, x, w, y in work]
                           for _ in range(copies - 1)]
 
-    def one_pass(ws):
+    def one_pass(ws, flags=None):
         for layer, sp, x, w, y in ws:
-            conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC)
+            conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC if flags is None else flags)
 
-    def all_passes():
+    def all_passes(flags=None):
         for ws in work_sets:
-            one_pass(ws)
+            one_pass(ws, flags)
 
     # launches per pass (our kernels only)
     _lib.lib.imconv_reset_launch_count()
@@ -593,6 +603,31 @@ def main(argv=None):
         t = torch.tensor([ms_rank], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # ---- the same step with the layers serialised (no IMCONV_FLAG_INDEPENDENT), same replays ----
+    serial_ms = None
+    if STATIC != SERIAL_FLAGS and graph is not None:
+        g_ser = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            all_passes(SERIAL_FLAGS)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g_ser, stream=stream):
+            all_passes(SERIAL_FLAGS)
+        g_ser.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for _ in range(replays):
+            g_ser.replay()
+        e1.record(cur)
+        torch.cuda.synchronize()
+        serial_ms = e0.elapsed_time(e1) / passes
+        if world > 1:
+            t = torch.tensor([serial_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            serial_ms = float(t.item())
+        del g_ser
     total_flops = sum(l.spec.flops for l in layers_full)  # all ranks together
     if shard_world != world:  # emulated: every rank assumed as fast as rank 0
         total_flops = total_flops_rank * shard_world
@@ -616,8 +651,8 @@ def main(argv=None):
     for layer, sp, x, w, y in work:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=side):
-            for _ in range(reps):
-                conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC)
+            for _ in range(reps):  # (each layer alone: repeated launches share y, so never overlapped)
+                conv_device(x, w, *sp.conv_args(), y=y, flags=_lib.FLAG_STATIC_FILTER)
         g.replay()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         evs[0].record()
@@ -749,6 +784,9 @@ def main(argv=None):
             **({"emulated_world": shard_world} if shard_world != world else {}),
             "run": {"cuda_graph": graph is not None, "passes_per_replay": copies, "replays": replays,
                     "timed_region_ms": region_ms_rank,
+                    "layer_overlap": STATIC != SERIAL_FLAGS,
+                    **({"value_layers_serialized": total_flops / (serial_ms / 1e3) / 1e12,
+                        "ms_per_step_layers_serialized": serial_ms} if serial_ms else {}),
                     **({"value_stem_c3": useful_value} if useful_value is not None else {})},
             "pct_of_peak": {"measured_burst": value / shard_world / (dtype_peak if dtype_peak == int8_peak
                                                                      else peaks.get("bf16_tflops", 1648.9)),

@@ -68,6 +68,14 @@ extern "C" {
                                      converted before the step): the kernel's filter loads then
                                      start before its programmatic-launch wait, overlapping the
                                      previous conv's tail.  Inputs are always ordered.         */
+#define IMCONV_FLAG_INDEPENDENT 256   /* the caller guarantees that no kernel still in flight on the
+                                     stream writes this launch's input or filter, or reads or
+                                     writes its output (independent convolutions, e.g. a sweep of
+                                     layers over their own buffers): the kernel then never waits
+                                     for the preceding grid -- its CTAs start computing on the SMs
+                                     the previous conv's tail leaves idle.  Implies
+                                     IMCONV_FLAG_STATIC_FILTER.  Stream order is otherwise kept:
+                                     a later launch without the flag still waits for this one.  */
 
 /*
  * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,

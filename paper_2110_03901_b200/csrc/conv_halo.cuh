@@ -42,7 +42,7 @@
 namespace imconv {
 
 struct HaloParams {
-    int b_early;  // 1: static filter -- warp 0 loads it before griddepcontrol.wait
+    int b_early;  // 1: static filter -- warp 0 loads it before griddepcontrol.wait; 2: no role waits
     int n, h, w, k;
     int r, s, ph, pw, dh, dw;
     int p, q;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     // PDL: setup above overlaps the previous kernel's tail; no global memory is
     // touched before every prerequisite grid has completed
     ptx::griddep_launch_dependents();
-    if (!(p.b_early && warp == 0)) ptx::griddep_wait();
+    if (p.b_early < 2 && !(p.b_early && warp == 0)) ptx::griddep_wait();
     const int rs = p.r * p.s;
 
     if (warp == 0) {
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                 ptx::tma_load_3d(smem_b + ((p.r - 1 - r) * p.s + s_) * Cfg::kBTap, &tmap_b, bfull, 0, t * Cfg::kBKE, 0,
                                  pol_w);
             }
-            if (p.b_early) ptx::griddep_wait();  // the input tiles depend on the previous grid
+            if (p.b_early == 1) ptx::griddep_wait();  // the input tiles depend on the previous grid
             // ---- input tiles: one 4-D box {128 B of channels, QP pixels, TR rows, 1 image} ----
             const uint64_t pol_a = ptx::policy_evict_normal();
             int stage = 0;

@@ -26,7 +26,7 @@
 namespace imconv {
 
 struct HaloStreamParams {
-    int b_early;  // 1: static filter -- the B producer (warp 3) starts before griddepcontrol.wait
+    int b_early;  // 1: static filter -- the B producer (warp 3) starts before griddepcontrol.wait; 2: no wait
     int n, h, w, c, k;
     int r, s, ph, pw, dh, dw;
     int p, q;
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                  "TMEM allocation outside the 512 columns", tmem_base, (Cfg::kTmemCols));
     // PDL: setup above overlaps the previous kernel's tail
     ptx::griddep_launch_dependents();
-    if (!(p.b_early && warp == 3)) ptx::griddep_wait();
+    if (p.b_early < 2 && !(p.b_early && warp == 3)) ptx::griddep_wait();
 
     if (warp == 0) {
         if (lane == 0) {

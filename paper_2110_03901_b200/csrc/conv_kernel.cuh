@@ -86,7 +86,8 @@ struct ConvParams {
                          //    tiled TMA boxes {128 B of channels, rows} (cheaper per operation than im2col)
     int dbg_flags;       // instrumentation builds only: 1 / 2 = load B / A on a CTA's first tile only
                          // (wrong results; measures what the operand stream costs)
-    int b_early;         // 1: the filter is not written by the preceding grid -- the B producers
+    int b_early;         // 2: independent launch -- no role waits for the preceding grid;
+                         // 1: the filter is not written by the preceding grid -- the B producers
                          //    start before griddepcontrol.wait (PDL) and prefetch their ring stages
 };
 
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     ptx::griddep_launch_dependents();
     // B producers touch nothing but the filter and shared memory: with a static
     // filter they fill their ring stages while the previous grid drains
-    if (!(p.b_early && (warp == 3 || warp == 8))) ptx::griddep_wait();
+    if (p.b_early < 2 && !(p.b_early && (warp == 3 || warp == 8))) ptx::griddep_wait();
     if (IMCONV_INSTRUMENT && threadIdx.x == 0) tl_stamp(p.dbg, tl_idx, 1);
 
     if (CG == 1 && STAGES >= 4 && p.a_gather && (warp == 0 || warp == 2)) {  // (>= 2 ring slots per gather warp)

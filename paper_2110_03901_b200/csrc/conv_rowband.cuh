@@ -37,7 +37,7 @@ constexpr int kProducers = 128;  // warps 0, 2, 3 and 8 gather the planes
 constexpr int kMaxEntPerThread = 4;  // sw * needed <= 512 plane pixels per input row
 
 struct RowbandParams {
-    int b_early;  // 1: static filter -- warp 0 loads it before griddepcontrol.wait
+    int b_early;  // 1: static filter -- warp 0 loads it before griddepcontrol.wait; 2: no role waits
     int n, h, w, k;
     int r, s, sh, sw, ph, pw, dh, dw;
     int p, q;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
     // PDL: setup above overlaps the previous kernel's tail; no global memory is
     // touched before every prerequisite grid has completed
     ptx::griddep_launch_dependents();
-    if (!(p.b_early && warp == 0)) ptx::griddep_wait();
+    if (p.b_early < 2 && !(p.b_early && warp == 0)) ptx::griddep_wait();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
                     }
         }
         __syncwarp();
-        if (p.b_early) ptx::griddep_wait();  // the planes read the previous grid's output
+        if (p.b_early == 1) ptx::griddep_wait();  // the planes read the previous grid's output
     }
     if (warp == 0 || warp == 2 || warp == 3 || warp == 8) {
         // ---- plane producers: cp.async 16-byte pixels into the stride-phase planes ----

@@ -153,6 +153,14 @@ CUtensorMapDataType tmap_dtype(int in_dtype) {
 
 int elem_bytes(int in_dtype) { return in_dtype == IMCONV_I8 ? 1 : 2; }
 
+// Programmatic-launch wait mode of the kernels' b_early parameter: 0 every role waits for the
+// preceding grid, 1 the filter loads start before the wait (IMCONV_FLAG_STATIC_FILTER), 2 no role
+// waits (IMCONV_FLAG_INDEPENDENT: nothing in flight touches this launch's buffers).
+int early_mode(int flags) {
+    if (flags & IMCONV_FLAG_INDEPENDENT) return 2;
+    return (flags & IMCONV_FLAG_STATIC_FILTER) ? 1 : 0;
+}
+
 // Conv kernels are launched with programmatic stream serialization (PDL): the
 // next kernel's CTAs may start their setup (barrier init, TMEM allocation,
 // tensor-map prefetch) on SMs this kernel has released, and block in
@@ -302,7 +310,7 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
     if (R * S == 1) return kNotApplicable;
     if (K % nc != 0 || !(K == 64 || K == 128 || K == 256) || (E == 1 && K < 128)) return kNotApplicable;
     HaloParams p{};
-    p.b_early = (a->flags & IMCONV_FLAG_STATIC_FILTER) ? 1 : 0;
+    p.b_early = early_mode(a->flags);
     p.n = static_cast<int>(a->n);
     p.h = static_cast<int>(a->h);
     p.w = static_cast<int>(a->w_);
@@ -456,7 +464,7 @@ int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cu
     if (R * S == 1 || !(K == 64 || K == 128)) return kNotApplicable;
     constexpr int HB = 2;
     HaloStreamParams p{};
-    p.b_early = (a->flags & IMCONV_FLAG_STATIC_FILTER) ? 1 : 0;
+    p.b_early = early_mode(a->flags);
     p.n = static_cast<int>(a->n);
     p.h = static_cast<int>(a->h);
     p.w = static_cast<int>(a->w_);
@@ -561,7 +569,7 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     const int BN = K <= 64 ? 64 : (K <= 128 ? 128 : 256);
     const int TP = 256 / BN;
     RowbandParams p{};
-    p.b_early = (a->flags & IMCONV_FLAG_STATIC_FILTER) ? 1 : 0;
+    p.b_early = early_mode(a->flags);
     p.n = static_cast<int>(a->n);
     p.h = static_cast<int>(a->h);
     p.w = static_cast<int>(a->w_);
@@ -1471,7 +1479,7 @@ int imconv_conv2d_nhwc(const imconv_conv_args *a, void *stream) {
         p.k_stages = plan.k_subs;
     }
     p.dbg_flags = g_debug_flags & 0xff;
-    p.b_early = (!cl && (a->flags & IMCONV_FLAG_STATIC_FILTER)) ? 1 : 0;
+    p.b_early = cl ? 0 : early_mode(a->flags);
 
     const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles;
     int grid = plan.grid;

@@ -636,3 +636,53 @@ def test_static_filter_dependent_chain():
             assert not torch.isnan(y).any(), (rep, i)
             assert torch.equal(y, ref), (rep, i)
             inp = y
+
+
+def test_independent_launches_overlap_exact():
+    """IMCONV_FLAG_INDEPENDENT: a sweep of independent convolutions over their own buffers (every
+    kernel family, split-K tails included) queued back to back in one CUDA graph with no
+    programmatic-launch wait, so each layer's CTAs start while the previous layer still runs.
+    Replayed several times into NaN-refilled outputs, every layer must equal a separate
+    serialised launch; and a flag-free launch queued after the sweep still waits for it."""
+    P = _P()
+    from paper_2110_03901_b200._kernels import conv_device
+    from paper_2110_03901_b200.core import ConvSpec
+    from paper_2110_03901_b200.traffic import plan
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(11)
+    sq = ConvSpec.square
+    sweep = [sq(16, 8, 224, 64, 7, stride=2, pad=3), sq(32, 64, 56, 64, 3, stride=1, pad=1),
+             sq(32, 64, 56, 256, 1), sq(64, 128, 28, 128, 3, stride=1, pad=1),
+             sq(256, 512, 7, 512, 3, stride=1, pad=1), sq(64, 256, 14, 1024, 1), sq(32, 512, 7, 512, 3, stride=1, pad=1)]
+    assert any(plan(sp).sk_split > 1 for sp in sweep)
+    xs, ws, ys, refs = [], [], [], []
+    for sp in sweep:
+        x = torch.randint(-2, 3, (sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev, generator=g).bfloat16()
+        w = torch.randint(-2, 3, (sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev, generator=g).bfloat16()
+        xs.append(x)
+        ws.append(w)
+        ys.append(torch.empty((sp.n, sp.h_o, sp.w_o, sp.c_o), device=dev, dtype=torch.float32))
+        refs.append(conv_device(x, w, *sp.conv_args(), out_dtype=torch.float32))
+    torch.cuda.synchronize()
+    flags = P._lib.FLAG_STATIC_FILTER | P._lib.FLAG_INDEPENDENT
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for sp, x, w, y in zip(sweep, xs, ws, ys):
+            conv_device(x, w, *sp.conv_args(), y=y, out_dtype=torch.float32, flags=flags)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        for sp, x, w, y in zip(sweep, xs, ws, ys):
+            conv_device(x, w, *sp.conv_args(), y=y, out_dtype=torch.float32, flags=flags)
+    total = torch.zeros((), device=dev, dtype=torch.float64)
+    for rep in range(20):
+        for y in ys:
+            y.fill_(float("nan"))
+        graph.replay()
+        # a flag-free consumer queued after the sweep: must see the last layer's finished output
+        total += ys[-1].double().sum()
+        torch.cuda.synchronize()
+        for i, (y, ref) in enumerate(zip(ys, refs)):
+            assert torch.equal(y, ref), (rep, i)
+    assert total.item() == 20 * refs[-1].double().sum().item()
