@@ -475,6 +475,11 @@ def main(argv=None):
     ap.add_argument("--no-traffic", action="store_true",
                     help="skip the in-run ncu DRAM-traffic measurement (report the committed figure if any)")
     ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--launch-order", default="sweep", choices=["sweep", "reverse"],
+                    help="order of the layers' launches inside the timed step (diagnostic)")
+    ap.add_argument("--planner-debug", type=lambda v: int(v, 0), default=0,
+                    help="diagnostic A/B only: host planner switches (imconv_debug_set_flags bits 16+); "
+                         "reported in the line's `run` object")
     ap.add_argument("--emulate-world", type=int, default=0,
                     help="diagnostic (1 process): run rank 0's shard of a W-rank job and report W x its "
                          "throughput, i.e. what the W-GPU run measures when every rank matches rank 0")
@@ -515,6 +520,10 @@ def main(argv=None):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     peaks, peak_kind = load_peaks()
+    if args.planner_debug:
+        if args.planner_debug & 0xffff:
+            raise SystemExit("--planner-debug takes host planner switches only (bits 16+)")
+        _lib.lib.imconv_debug_set_flags(args.planner_debug)
 
     # ---- per-rank shard of every layer (contiguous images; no collective) ----
     work = []
@@ -538,7 +547,8 @@ def main(argv=None):
                           for _ in range(copies - 1)]
 
     def one_pass(ws, flags=None):
-        for layer, sp, x, w, y in ws:
+        order = ws[::-1] if args.launch_order == "reverse" else ws
+        for layer, sp, x, w, y in order:
             conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC if flags is None else flags)
 
     def all_passes(flags=None):
@@ -785,6 +795,7 @@ def main(argv=None):
             "run": {"cuda_graph": graph is not None, "passes_per_replay": copies, "replays": replays,
                     "timed_region_ms": region_ms_rank,
                     "layer_overlap": STATIC != SERIAL_FLAGS,
+                    **({"planner_debug": hex(args.planner_debug)} if args.planner_debug else {}),
                     **({"value_layers_serialized": total_flops / (serial_ms / 1e3) / 1e12,
                         "ms_per_step_layers_serialized": serial_ms} if serial_ms else {}),
                     **({"value_stem_c3": useful_value} if useful_value is not None else {})},

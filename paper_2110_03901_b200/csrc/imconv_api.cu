@@ -44,6 +44,7 @@ constexpr int kDbgNoHaloStack = 1 << 25;  // halo kernel: one sub-block per bloc
 constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep the generic kernel
 constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-stationary layout
 constexpr int kDbgNoPairSplit = 1 << 28;  // CTA pairs never split the tail wave's k-loops
+constexpr int kDbgThrNoPair = 1 << 24;    // throughput mode: sub-wave layers keep single CTAs
 constexpr int kDbgStreamK = 1 << 29;      // stream-K the last two waves (measured slower: opt-in, see below)
 
 // Split-K ticket counters (conv_kernel.cuh sk_arrive): one per tail tile, never
@@ -896,7 +897,9 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
         // whole tile (get_unit): k-loops of >= 24 stages gain (tools/ab_layers.py: s5 3x3 at
         // N = 256 49.6 -> 41.1 us, s5 1x1a (32 stages) 26.0 -> 23.9; 16-stage 1x1 layers lose ~8%).
         constexpr int kSkMaxSplit = 5, kSkMinStages = 36, kSkMinStagesHidden = 24;
-        const bool sub_wave = g->tiles < g0 && k_st >= kSkMinStages;
+        // (throughput mode, IMCONV_FLAG_INDEPENDENT: the idle SMs of a sub-wave layer run the next
+        // launch, so a split that spends SM time on the partials' round trip does not pay)
+        const bool sub_wave = g->tiles < g0 && k_st >= kSkMinStages && !(a->flags & IMCONV_FLAG_INDEPENDENT);
         const bool short_tail = g->tiles >= g0 && tail > 0 && 2 * tail <= g0 && k_st >= kSkMinStagesHidden;
         if (sub_wave || short_tail) {
             const int Sk = static_cast<int>(std::min<long long>(
@@ -979,6 +982,16 @@ int plan_generic(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, Gener
             GenericPlan h;
             if (plan_generic_bn(a, P, Q, sms, 256, -1, &h, true) == 0 && h.use_pair) *g = h;
         }
+        return 0;
+    }
+    if (a->flags & IMCONV_FLAG_INDEPENDENT) {
+        // Throughput mode (sub-wave, independent launch): the SMs this layer leaves idle run the
+        // next launch, so the block shape minimises SM time (CTAs x per-CTA time), not this
+        // layer's latency: the largest blocks, CTA pairs when a pair block exists, no split.
+        GenericPlan h;
+        if (!(g_debug_flags & kDbgThrNoPair) && !(a->flags & IMCONV_FLAG_SINGLE_CTA) &&
+            plan_generic_bn(a, P, Q, sms, 256, -1, &h, true) == 0 && h.use_pair)
+            *g = h;
         return 0;
     }
     GenericPlan h;

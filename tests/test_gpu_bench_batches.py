@@ -55,6 +55,17 @@ EXPECTED_BRANCHES = {
 
 @pytest.mark.parametrize("n", [256, 128, 64, 32])
 def test_resnet50_shapes_at_shard_batch(n):
+    _check_shapes_at_shard_batch(n, independent=False)
+
+
+@pytest.mark.parametrize("n", [64, 32])
+def test_resnet50_shapes_throughput_mode(n):
+    """bench.py launches the sweep with IMCONV_FLAG_INDEPENDENT: sub-wave layers then take the
+    throughput-mode plans (CTA pairs, no split-K) -- checked against the oracle the same way."""
+    _check_shapes_at_shard_batch(n, independent=True)
+
+
+def _check_shapes_at_shard_batch(n, independent):
     import paper_2110_03901_b200 as P
     from oracle import oracle as O
     from paper_2110_03901_b200._kernels import conv_device
@@ -67,9 +78,10 @@ def test_resnet50_shapes_at_shard_batch(n):
             continue
         seen.add(layer.spec)
         sp = layer.spec
-        branches.add(plan(sp).branch)
+        flags = P._lib.FLAG_STATIC_FILTER | (P._lib.FLAG_INDEPENDENT if independent else 0)
+        branches.add(plan(sp, flags=flags).branch)
         x, w = _operands(layer, sp, 100 + li, dev)
-        y = conv_device(x, w, *sp.conv_args(), flags=P._lib.FLAG_STATIC_FILTER)  # bench.py's call
+        y = conv_device(x, w, *sp.conv_args(), flags=flags)  # bench.py's call
         torch.cuda.synchronize()
         wf = w.float().cpu().numpy()
         for i in sorted({0, n // 2, n - 1}):
@@ -77,6 +89,10 @@ def test_resnet50_shapes_at_shard_batch(n):
             err = _norm_err(y[i:i + 1].float().cpu().numpy(), ref)
             assert err <= REL_TOL, (n, layer.name, i, err)
         del x, w, y
+    if independent:
+        assert not any("split" in b for b in branches if "x" in b and n <= 64), branches
+        assert "generic 256x256 pair" in branches
+        return
     missing = EXPECTED_BRANCHES[n] - branches
     assert not missing, (n, missing, branches)
 
