@@ -122,6 +122,8 @@ def measure_traffic(args, launches: int, timeout_s: float = 420.0):
     finally:
         if os.path.exists(log):
             os.remove(log)
+    if len(rows) < 2:  # e.g. this bench itself runs under ncu (nested profiling is refused)
+        return None, "ncu child produced no launch rows", None
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1.0, "usecond": 1e3,
              "msecond": 1e6}
     h = rows[0]

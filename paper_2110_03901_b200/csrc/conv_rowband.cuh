@@ -65,8 +65,7 @@ struct RowbandParams {
     int dbg_flags;            // instrumentation: 1 = epilogue skips TMEM/stores, 2 = producer skips copies,
                               // 4 = one MMA per (row, filter row) instead of npairs, 8 = issuer skips MMAs,
                               // 16 = producer skips the proxy fence, 32 = one full-barrier arrive per warp,
-                              // 64 / 128 = epilogue / producer waits back off with nanosleep, 1 << 28 = no output stores,
-                              // 1 << 30 = plane producers keep the identity lane mapping (A/B of the permutation)
+                              // 64 / 128 = epilogue / producer waits back off with nanosleep, 1 << 28 = no output stores
 };
 
 // instrumentation: cycles spent in a blocking wait, accumulated per role
@@ -179,14 +178,10 @@ __global__ void __launch_bounds__(kThreadsRowband, 1)
         // (LSU path: a 16-byte TMA element costs as much TMA time as a 128-byte
         // one, so strided 16-byte pixels are gathered by threads instead; warp 0
         // joins after issuing the resident-filter load)
-        // lane -> entry permutation inside each warp's 32 consecutive input columns: with
-        // sw stride-phase planes, lanes [l*32/sw, (l+1)*32/sw) take plane l's columns, so every
-        // 8-lane quarter writes 128 contiguous bytes of one plane (no 2-way bank conflict between
-        // the planes' interleaved slots; the warp still reads the same 512 contiguous bytes)
-        const int lpp = (32 % p.sw == 0 && !(p.dbg_flags & (1 << 30))) ? 32 / p.sw : 32;  // lanes per plane
-        const int lperm = lpp == 32 ? static_cast<int>(lane)
-                                    : (static_cast<int>(lane) % lpp) * p.sw + static_cast<int>(lane) / lpp;
-        const int t = (warp == 0 ? 0 : warp == 8 ? 3 : warp - 1) * 32 + lperm;
+        // consecutive lanes copy consecutive input pixels (each 8-lane phase reads one 128-byte
+        // line); the planes' pitch is 128 / sw bytes off a multiple of 128 (host), so the phase's
+        // sw interleaved plane slots land on disjoint banks: one shared-memory wavefront per phase
+        const int t = (warp == 0 ? 0 : warp == 8 ? 3 : warp - 1) * 32 + static_cast<int>(lane);
         const int entries = (IMCONV_INSTRUMENT && (p.dbg_flags & 2)) ? 0 : p.sw * p.needed;
         const uint32_t a0 = ptx::smem_u32(smem_a);
         // this thread's (plane, pixel) entries, fixed for the whole kernel:

@@ -45,6 +45,7 @@ constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep th
 constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-stationary layout
 constexpr int kDbgNoPairSplit = 1 << 28;  // CTA pairs never split the tail wave's k-loops
 constexpr int kDbgThrNoPair = 1 << 24;    // throughput mode: sub-wave layers keep single CTAs
+constexpr int kDbgPlanePitch128 = 1 << 20;  // row-band planes at a 128-byte-multiple pitch (A/B)
 constexpr int kDbgStreamK = 1 << 29;      // stream-K the last two waves (measured slower: opt-in, see below)
 
 // Split-K ticket counters (conv_kernel.cuh sk_arrive): one per tail tile, never
@@ -604,7 +605,11 @@ int try_rowband(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaSt
     p.x = static_cast<const uint8_t *>(a->x);
     p.dbg = g_debug_buf;
     p.dbg_flags = g_debug_flags;
-    p.plane_bytes = ((plane_pix * 16 + 127) / 128) * 128;
+    // plane pitch: 128 / sw bytes past a multiple of 128, so the sw planes' slots written by one
+    // 8-lane copy phase fall on disjoint banks (a 128-byte multiple made every phase 2-way
+    // conflicted: 2.9 M excess wavefronts per stem launch); descriptors need 16-byte alignment only
+    p.plane_bytes = ((plane_pix * 16 + 127) / 128) * 128 +
+                    ((p.sw > 1 && 8 % p.sw == 0 && !(g_debug_flags & kDbgPlanePitch128)) ? 128 / p.sw : 0);
     p.row_bytes_planes = p.sw * p.plane_bytes;
     const int rows_needed = (TP - 1) * p.sh + (R - 1) * p.dh + 1;
     p.npairs = (S + 1) / 2;
@@ -897,10 +902,12 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
         // whole tile (get_unit): k-loops of >= 24 stages gain (tools/ab_layers.py: s5 3x3 at
         // N = 256 49.6 -> 41.1 us, s5 1x1a (32 stages) 26.0 -> 23.9; 16-stage 1x1 layers lose ~8%).
         constexpr int kSkMaxSplit = 5, kSkMinStages = 36, kSkMinStagesHidden = 24;
-        // (throughput mode, IMCONV_FLAG_INDEPENDENT: the idle SMs of a sub-wave layer run the next
-        // launch, so a split that spends SM time on the partials' round trip does not pay)
-        const bool sub_wave = g->tiles < g0 && k_st >= kSkMinStages && !(a->flags & IMCONV_FLAG_INDEPENDENT);
-        const bool short_tail = g->tiles >= g0 && tail > 0 && 2 * tail <= g0 && k_st >= kSkMinStagesHidden;
+        // Throughput mode (IMCONV_FLAG_INDEPENDENT): a layer's idle SMs -- below one wave or in its
+        // last wave -- run the next launch, so splitting only adds the partials' round trip
+        // (measured: 2-GPU shard of the cfg4 sweep 1598 -> 1679 TFLOP/s without split tails).
+        const bool thr = (a->flags & IMCONV_FLAG_INDEPENDENT) != 0;
+        const bool sub_wave = g->tiles < g0 && k_st >= kSkMinStages && !thr;
+        const bool short_tail = g->tiles >= g0 && tail > 0 && 2 * tail <= g0 && k_st >= kSkMinStagesHidden && !thr;
         if (sub_wave || short_tail) {
             const int Sk = static_cast<int>(std::min<long long>(
                 {g0 / tail, static_cast<long long>(k_st / 4), kSkMaxSplit}));

@@ -14,7 +14,7 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 for W in 2 4 8; do
   timeout 600 python bench.py --emulate-world $W --no-e2e --no-cpu --layers-json gpurun_out/layers_${TAG}_emu$W.json > gpurun_out/bench_${TAG}_emu$W.json 2>&1; echo "emu$W rc=$?"
 done
-CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph"
+CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph --no-traffic"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"conv_" -s 53 -c 53 --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch.log 2>&1
