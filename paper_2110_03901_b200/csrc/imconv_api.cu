@@ -46,7 +46,8 @@ constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-
 constexpr int kDbgNoPairSplit = 1 << 28;  // CTA pairs never split the tail wave's k-loops
 constexpr int kDbgThrNoPair = 1 << 24;    // throughput mode: sub-wave layers keep single CTAs
 constexpr int kDbgPlanePitch128 = 1 << 20;  // row-band planes at a 128-byte-multiple pitch (A/B)
-constexpr int kDbgStreamK = 1 << 29;      // stream-K the last two waves (measured slower: opt-in, see below)
+constexpr int kDbgStreamK = 1 << 29;
+constexpr int kDbgHaloStreamSingle = 1 << 30;  // halo-stream K = 128 layers keep single CTAs (A/B of the pair)      // stream-K the last two waves (measured slower: opt-in, see below)
 
 // Split-K ticket counters (conv_kernel.cuh sk_arrive): one per tail tile, never
 // cleared (they only grow, in steps that leave a multiple of kSkRound between
@@ -370,7 +371,8 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
         cuuint64_t gdim[3] = {static_cast<cuuint64_t>(nc), static_cast<cuuint64_t>(R * S * C),
                               static_cast<cuuint64_t>(K / nc)};
         cuuint64_t gstride[2] = {static_cast<cuuint64_t>(K * E), static_cast<cuuint64_t>(nc * E)};
-        cuuint32_t box[3] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(K / nc)};
+        cuuint32_t box[3] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(nc),
+                             static_cast<cuuint32_t>(K / nc)};
         cuuint32_t es[3] = {1, 1, 1};
         if (g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 3, const_cast<void *>(a->w), gdim, gstride, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -419,14 +421,14 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
 #undef IMCONV_HALO
 }
 
-template <int ELEM, int OUT, int BN>
+template <int ELEM, int OUT, int BN, int CG = 1>
 int launch_halo_stream(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const HaloStreamParams &p,
                        int smem, int grid, cudaStream_t st) {
-    auto kern = conv_halo_stream_kernel<ELEM, OUT, BN, 2>;
+    auto kern = conv_halo_stream_kernel<ELEM, OUT, BN, 2, CG>;
     static std::atomic<unsigned long long> attr_done{0};
-    const cudaError_t attr_err = ensure_attrs(attr_done, kern, kMaxDynSmem, false);
+    const cudaError_t attr_err = ensure_attrs(attr_done, kern, kMaxDynSmem, CG == 2);
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    cudaError_t le = launch_pdl(kern, grid, kThreadsGeneric, smem, st, 1, ta, tb, ty, p);
+    cudaError_t le = launch_pdl(kern, grid, kThreadsGeneric, smem, st, CG, ta, tb, ty, p);
     if (le != cudaSuccess) return static_cast<int>(le);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
@@ -489,14 +491,21 @@ int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cu
     p.tiles = static_cast<long long>(p.n) * p.p_tiles;
     if (a->num_ctas <= 0 && !halo_stream_wave_ok(p.tiles, a->n * P * Q, sms)) return kNotApplicable;
     p.chunks = static_cast<int>(a->c * E / 128);
+    // K = 128: a CTA pair runs two blocks with M = 256 MMAs, each CTA holding half of every filter
+    // slice (one 64-column atom): 6 instead of 8 KB of operands per SM per 16-deep MMA
+    // (below one wave of blocks the single-CTA kernel wins: s3 3x3 at N = 32 9.9 vs 10.4 us)
+    const int cg = (K == 128 && !(a->flags & IMCONV_FLAG_SINGLE_CTA) && !(g_debug_flags & kDbgHaloStreamSingle) &&
+                    (a->num_ctas <= 0 || a->num_ctas % 2 == 0) && p.tiles >= sms)
+                       ? 2
+                       : 1;
     p.a_box_bytes = p.tr * p.qp * 128;
     const int rows_read =
         std::max(p.tr * p.qp, (HB - 1) * p.tpr * p.qp + 128 + (R - 1) * p.dh * p.qp + (S - 1) * p.dw);
     p.a_slot_bytes = (rows_read * 128 + 1023) / 1024 * 1024;
-    const int b_stage = K * 128;
+    const int b_stage = K * 128 / cg;
     const int fixed = 2 * kBM * 128 + 1024 /*align*/ + 1024 /*barriers*/;
-    p.na = 2;
-    p.nb = std::min(8, (kMaxDynSmem - fixed - p.na * p.a_slot_bytes) / b_stage);
+    p.na = 2;  // (3 input slots with the pair's 8 KB filter stages: 47.1 -> 47.4 us, not kept)
+    p.nb = std::min(cg == 2 ? 12 : 8, (kMaxDynSmem - fixed - p.na * p.a_slot_bytes) / b_stage);
     if (p.nb < 3) return kNotApplicable;
     const int smem = fixed + p.na * p.a_slot_bytes + p.nb * b_stage;
 
@@ -524,7 +533,8 @@ int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cu
         cuuint64_t gdim[3] = {static_cast<cuuint64_t>(nc), static_cast<cuuint64_t>(R * S * C),
                               static_cast<cuuint64_t>(K / nc)};
         cuuint64_t gstride[2] = {static_cast<cuuint64_t>(K * E), static_cast<cuuint64_t>(nc * E)};
-        cuuint32_t box[3] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(K / nc)};
+        cuuint32_t box[3] = {static_cast<cuuint32_t>(nc), static_cast<cuuint32_t>(nc),
+                             static_cast<cuuint32_t>(K / nc / cg)};
         cuuint32_t es[3] = {1, 1, 1};
         if (g_encode_tiled(&tb, tmap_dtype(a->in_dtype), 3, const_cast<void *>(a->w), gdim, gstride, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -549,11 +559,16 @@ int try_halo_stream(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cu
             return IMCONV_ETMAP;
     }
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
-    if (grid > p.tiles) grid = static_cast<int>(p.tiles);
+    if (cg == 2) {  // one pair per two blocks, whole clusters
+        grid = static_cast<int>(std::min<long long>(grid, 2 * ((p.tiles + 1) / 2))) & ~1;
+    } else if (grid > p.tiles) {
+        grid = static_cast<int>(p.tiles);
+    }
     const bool f32 = a->out_dtype == IMCONV_F32;
 #define IMCONV_HS(EL, OUTK)                                                                   \
-    return K == 64 ? launch_halo_stream<EL, OUTK, 64>(ta, tb, ty, p, smem, grid, st)          \
-                   : launch_halo_stream<EL, OUTK, 128>(ta, tb, ty, p, smem, grid, st);
+    return K == 64    ? launch_halo_stream<EL, OUTK, 64>(ta, tb, ty, p, smem, grid, st)        \
+           : cg == 2  ? launch_halo_stream<EL, OUTK, 128, 2>(ta, tb, ty, p, smem, grid, st)    \
+                      : launch_halo_stream<EL, OUTK, 128>(ta, tb, ty, p, smem, grid, st);
     if (a->in_dtype == IMCONV_BF16) {
         if (f32) { IMCONV_HS(ELEM_BF16, OUT_F32) } else { IMCONV_HS(ELEM_BF16, OUT_BF16) }
     } else {

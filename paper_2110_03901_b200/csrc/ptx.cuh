@@ -298,6 +298,14 @@ __device__ __forceinline__ void tma_load_3d_2sm(void *dst, const CUtensorMap *m,
         "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_4d_2sm(void *dst, const CUtensorMap *m, uint32_t bar_cluster, int32_t c0,
+                                                int32_t c1, int32_t c2, int32_t c3, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_im2col_4d_2sm(void *dst, const CUtensorMap *m, uint32_t bar_cluster,
                                                        int32_t c, int32_t w, int32_t h, int32_t n, uint16_t off_w,
                                                        uint16_t off_h, uint64_t policy) {
