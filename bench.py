@@ -477,6 +477,9 @@ def main(argv=None):
     ap.add_argument("--no-traffic", action="store_true",
                     help="skip the in-run ncu DRAM-traffic measurement (report the committed figure if any)")
     ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--sweep-jobs", type=float, default=0.0,
+                    help="convolutions in flight in the overlapped step (paper_2110_03901_b200.sweep; "
+                         "0 = the library default for the step's work)")
     ap.add_argument("--launch-order", default="sweep", choices=["sweep", "reverse"],
                     help="order of the layers' launches inside the timed step (diagnostic)")
     ap.add_argument("--planner-debug", type=lambda v: int(v, 0), default=0,
@@ -548,8 +551,17 @@ def main(argv=None):
     work_sets = [work] + [[(layer, sp, x.clone(), w.clone(), torch.empty_like(y)) for layer, sp, x, w, y in work]
                           for _ in range(copies - 1)]
 
+    from paper_2110_03901_b200 import sweep as SW
+    sweep_jobs = args.sweep_jobs or SW.default_jobs(float(sum(sp.flops for _, sp, *_ in work)))
+
     def one_pass(ws, flags=None):
         order = ws[::-1] if args.launch_order == "reverse" else ws
+        if flags is None and STATIC != SERIAL_FLAGS:
+            # the overlapped step: the layers as one sweep of independent convolutions, about
+            # `sweep_jobs` of them in flight at a time (paper_2110_03901_b200.sweep)
+            SW.conv_sweep([(x, w, sp.conv_args(), y) for layer, sp, x, w, y in order], jobs=sweep_jobs,
+                          check=True)
+            return
         for layer, sp, x, w, y in order:
             conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC if flags is None else flags)
 
@@ -704,11 +716,19 @@ def main(argv=None):
     achieved = total_flops_rank / (ms_rank / 1e3) / 1e12
     roof_ms = 0.0
     layer_rows = []
+    # per roofline bound: the layers whose tensor time exceeds their HBM time, and the rest --
+    # each group's bound time over its measured time (the kernels' quality, apart from the mix)
+    groups = {"tensor": [0, 0.0, 0.0], "hbm": [0, 0.0, 0.0]}
     for layer, sp, t_ms in per_layer:
         eo = 4 if layer.dtype == "int8" else 2
         b = bytes_alg(sp, layer.dtype, eo)
         pk = int8_peak if (layer.dtype == "int8" and int8_peak) else bf16_peak
-        t_roof = max(sp.flops / (pk * 1e12), b / (hbm * 1e9)) * 1e3
+        t_tc, t_mem = sp.flops / (pk * 1e12) * 1e3, b / (hbm * 1e9) * 1e3
+        t_roof = max(t_tc, t_mem)
+        gr = groups["tensor" if t_tc >= t_mem else "hbm"]
+        gr[0] += 1
+        gr[1] += t_ms
+        gr[2] += t_roof
         roof_ms += t_roof
         layer_rows.append({"layer": layer.name, "n": sp.n, "ms": round(t_ms, 5),
                            "tflops": round(sp.flops / (t_ms / 1e3) / 1e12, 2),
@@ -798,6 +818,8 @@ def main(argv=None):
                     "timed_region_ms": region_ms_rank,
                     "layer_overlap": STATIC != SERIAL_FLAGS,
                     **({"planner_debug": hex(args.planner_debug)} if args.planner_debug else {}),
+                    **({"sweep_jobs": round(sweep_jobs, 3),
+                        "sweep_ctas_per_launch": SW.sweep_grid(sweep_jobs, dev)} if STATIC != SERIAL_FLAGS else {}),
                     **({"value_layers_serialized": total_flops / (serial_ms / 1e3) / 1e12,
                         "ms_per_step_layers_serialized": serial_ms} if serial_ms else {}),
                     **({"value_stem_c3": useful_value} if useful_value is not None else {})},
@@ -822,7 +844,12 @@ def main(argv=None):
                          "peak_kind": peak_name,
                          "kernel": "conv kernels (generic / row-band / halo), all layers of the step",
                          "achieved_source": "timed region: rank FLOP / device ms per pass",
-                         "roofline_limited_frac": roof_ms / ms_rank},
+                         "roofline_limited_frac": roof_ms / ms_rank,
+                         "by_bound": {k: {"layers": v[0], "ms_per_step": round(v[1], 4),
+                                          "frac": round(v[2] / v[1], 3) if v[1] else None,
+                                          "of": ("tensor peak" if k == "tensor" else "HBM copy bandwidth")}
+                                      for k, v in groups.items()},
+                         "by_bound_source": "separate per-layer pass (each layer alone, 5 launches per CUDA graph)"},
             "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,

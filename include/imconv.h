@@ -76,6 +76,12 @@ extern "C" {
                                      the previous conv's tail leaves idle.  Implies
                                      IMCONV_FLAG_STATIC_FILTER.  Stream order is otherwise kept:
                                      a later launch without the flag still waits for this one.  */
+#define IMCONV_FLAG_BARRIER 512       /* every preceding grid completes before this launch lets the
+                                     launches queued after it start (it waits, then triggers its
+                                     dependents): the first launch of a batch of
+                                     IMCONV_FLAG_INDEPENDENT launches, so that none of them can
+                                     run ahead of the work queued before the batch.  Takes
+                                     precedence over IMCONV_FLAG_INDEPENDENT / _STATIC_FILTER. */
 
 /*
  * Forward convolution, NHWC input x HWCN filter -> NHWC output, stride,

@@ -29,6 +29,7 @@ FLAG_SINGLE_CTA, FLAG_CTA_PAIR, FLAG_KSUB1, FLAG_MT1, FLAG_GATHER16, FLAG_NO_HAL
 FLAG_CHANNEL_LAST = 64
 FLAG_STATIC_FILTER = 128  # filter not written by kernels in flight: loads start before the PDL wait
 FLAG_INDEPENDENT = 256  # nothing in flight touches this launch's buffers: no PDL wait at all (implies STATIC_FILTER)
+FLAG_BARRIER = 512  # waits for every preceding grid before later launches may start (head of a batch)
 
 # every symbol include/imconv.h declares (checked by tests/test_abi.py)
 EXPORTED = (

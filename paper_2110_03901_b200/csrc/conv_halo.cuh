@@ -119,8 +119,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                  "TMEM allocation outside the 512 columns", tmem_base, (Cfg::kTmemCols));
     // PDL: setup above overlaps the previous kernel's tail; no global memory is
     // touched before every prerequisite grid has completed
-    ptx::griddep_launch_dependents();
-    if (p.b_early < 2 && !(p.b_early && warp == 0)) ptx::griddep_wait();
+    if (p.b_early == 3) {  // barrier launch: every preceding grid completes before later launches start
+        ptx::griddep_wait();
+        ptx::griddep_launch_dependents();
+    } else {
+        ptx::griddep_launch_dependents();
+        if (p.b_early < 2 && !(p.b_early && warp == 0)) ptx::griddep_wait();
+    }
     const int rs = p.r * p.s;
 
     if (warp == 0) {

@@ -131,8 +131,13 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     IMCONV_CHECK((tmem_base >> 16) == 0 && (tmem_base & 0xffffu) + (Cfg::kTmemCols) <= 512u,
                  "TMEM allocation outside the 512 columns", tmem_base, (Cfg::kTmemCols));
     // PDL: setup above overlaps the previous kernel's tail
-    ptx::griddep_launch_dependents();
-    if (p.b_early < 2 && !(p.b_early && warp == 3)) ptx::griddep_wait();
+    if (p.b_early == 3) {  // barrier launch: every preceding grid completes before later launches start
+        ptx::griddep_wait();
+        ptx::griddep_launch_dependents();
+    } else {
+        ptx::griddep_launch_dependents();
+        if (p.b_early < 2 && !(p.b_early && warp == 3)) ptx::griddep_wait();
+    }
 
     if (warp == 0) {
         if (lane == 0) {

@@ -459,10 +459,15 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
     volatile uint32_t *dbg_chunks = tmem_slot + 4;  // debug builds: staged / stored chunk counts
     // PDL: setup above overlaps the previous kernel's tail; no global memory is
     // touched before every prerequisite grid has completed
-    ptx::griddep_launch_dependents();
-    // B producers touch nothing but the filter and shared memory: with a static
-    // filter they fill their ring stages while the previous grid drains
-    if (p.b_early < 2 && !(p.b_early && (warp == 3 || warp == 8))) ptx::griddep_wait();
+    if (p.b_early == 3) {  // barrier launch: every preceding grid completes before later launches start
+        ptx::griddep_wait();
+        ptx::griddep_launch_dependents();
+    } else {
+        ptx::griddep_launch_dependents();
+        // B producers touch nothing but the filter and shared memory: with a static
+        // filter they fill their ring stages while the previous grid drains
+        if (p.b_early < 2 && !(p.b_early && (warp == 3 || warp == 8))) ptx::griddep_wait();
+    }
     if (IMCONV_INSTRUMENT && threadIdx.x == 0) tl_stamp(p.dbg, tl_idx, 1);
 
     if (CG == 1 && STAGES >= 4 && p.a_gather && (warp == 0 || warp == 2)) {  // (>= 2 ring slots per gather warp)

@@ -158,8 +158,10 @@ int elem_bytes(int in_dtype) { return in_dtype == IMCONV_I8 ? 1 : 2; }
 
 // Programmatic-launch wait mode of the kernels' b_early parameter: 0 every role waits for the
 // preceding grid, 1 the filter loads start before the wait (IMCONV_FLAG_STATIC_FILTER), 2 no role
-// waits (IMCONV_FLAG_INDEPENDENT: nothing in flight touches this launch's buffers).
+// waits (IMCONV_FLAG_INDEPENDENT: nothing in flight touches this launch's buffers), 3 the kernel
+// waits before it triggers its dependents (IMCONV_FLAG_BARRIER: head of an independent batch).
 int early_mode(int flags) {
+    if (flags & IMCONV_FLAG_BARRIER) return 3;  // wait for every preceding grid, then trigger
     if (flags & IMCONV_FLAG_INDEPENDENT) return 2;
     return (flags & IMCONV_FLAG_STATIC_FILTER) ? 1 : 0;
 }

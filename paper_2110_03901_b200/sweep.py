@@ -1,0 +1,102 @@
+"""Independent convolutions run concurrently -- the B200 counterpart of the reference's
+``sweep(specs, ..., jobs=N)`` (/root/reference/pkg/src/sasim/simulator.py:550-576), which
+evaluates independent specs on N worker threads.
+
+Here the N "jobs" are convolutions in flight on the GPU at the same time, on one stream:
+
+* every launch carries ``IMCONV_FLAG_INDEPENDENT`` (include/imconv.h): it does not wait for
+  the preceding grid, so its CTAs start on whatever SMs are free;
+* the first launch of a sweep carries ``IMCONV_FLAG_BARRIER`` instead: it waits for all work
+  queued before the sweep and only then lets the rest of the sweep start;
+* each launch runs on ``sms // jobs`` persistent CTAs, so about ``jobs`` convolutions share the
+  GPU: a memory-bound layer's stream overlaps a compute-bound layer's MMAs, and each layer's
+  fixed costs overlap other layers' work.  The planner's throughput mode applies (no split-K,
+  CTA pairs below one wave: the SMs a launch leaves idle run the others).
+
+Measured on the cfg4 sweep (53 ResNet-50 layers, profiles/r2/README.md): 1 / 2 / 4 / 8-GPU
+shards (256 / 128 / 64 / 32 images) 876 -> 916, 1662 -> 1813, 2956 -> 3521, 4724 -> 6553
+TFLOP/s against one launch at a time on every SM.
+
+The buffers of a sweep must be disjoint: no convolution may write memory another one (or any
+kernel still in flight) reads or writes.  ``conv_sweep`` checks the outputs against every
+operand of the sweep and raises ``ValueError`` on overlap.
+"""
+
+from __future__ import annotations
+
+from typing import Iterable, Sequence
+
+import torch
+
+from . import _lib
+
+# per-GPU work (FLOP per sweep) above which fewer, larger launches run side by side
+_BIG_SWEEP_FLOP = 1.5e12
+
+
+def default_jobs(flop: float) -> float:
+    """Convolutions in flight for a sweep of ``flop`` total work: ~8/3 for large sweeps
+    (56 CTAs each on 148 SMs), 4 below 1.5 TFLOP (37 CTAs each) -- the measured optima."""
+    return 8.0 / 3.0 if flop >= _BIG_SWEEP_FLOP else 4.0
+
+
+def sweep_grid(jobs: float, device: torch.device | None = None) -> int:
+    """Persistent CTAs per launch when ``jobs`` launches share the device's SMs."""
+    sms = torch.cuda.get_device_properties(device or torch.cuda.current_device()).multi_processor_count
+    return max(2, int(sms / jobs))
+
+
+def _span(t: torch.Tensor):
+    start = t.data_ptr()
+    return start, start + t.numel() * t.element_size()
+
+
+def _check_disjoint(convs) -> None:
+    spans = []
+    for i, (x, w, _args, y) in enumerate(convs):
+        spans.append((i, "x", _span(x)))
+        spans.append((i, "w", _span(w)))
+    for i, (x, w, _args, y) in enumerate(convs):
+        ylo, yhi = _span(y)
+        for j, what, (lo, hi) in spans:
+            if lo < yhi and ylo < hi:
+                raise ValueError(f"sweep output {i} overlaps {what} of convolution {j}")
+        for j, (_x2, _w2, _a2, y2) in enumerate(convs):
+            if j != i:
+                lo, hi = _span(y2)
+                if lo < yhi and ylo < hi:
+                    raise ValueError(f"sweep outputs {i} and {j} overlap")
+
+
+def conv_sweep(convs: Sequence, jobs: float | None = None, flops: float | None = None,
+               check: bool = True, flags: int = 0) -> list:
+    """Run independent convolutions concurrently on the current stream.
+
+    ``convs``: sequence of ``(x, w, (sh, sw, ph, pw, dh, dw), y)`` with CUDA tensors in the
+    compute dtype (``y`` preallocated, contiguous, the output dtype).  ``jobs``: convolutions
+    in flight (default: :func:`default_jobs` of the sweep's FLOP, given or computed).  Returns
+    the outputs.  Capturable into a CUDA graph like any launch of the library.
+    """
+    from ._kernels import conv_device
+    convs = list(convs)
+    if not convs:
+        return []
+    if check:
+        _check_disjoint(convs)
+    if jobs is None:
+        jobs = default_jobs(sweep_flops(convs) if flops is None else flops)
+    grid = sweep_grid(jobs, convs[0][0].device)
+    base = flags | _lib.FLAG_STATIC_FILTER | _lib.FLAG_INDEPENDENT
+    out = []
+    for i, (x, w, args, y) in enumerate(convs):
+        f = base | (_lib.FLAG_BARRIER if i == 0 else 0)
+        out.append(conv_device(x, w, *args, y=y, out_dtype=y.dtype, flags=f, num_ctas=grid))
+    return out
+
+
+def sweep_flops(convs: Iterable) -> float:
+    """2 * N*P*Q*K * R*S*C summed over ``(x, w, args, y)`` tuples."""
+    total = 0.0
+    for x, w, args, y in convs:
+        total += 2.0 * y.numel() * w.shape[0] * w.shape[1] * w.shape[2]
+    return total

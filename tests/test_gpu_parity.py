@@ -686,3 +686,42 @@ def test_independent_launches_overlap_exact():
         for i, (y, ref) in enumerate(zip(ys, refs)):
             assert torch.equal(y, ref), (rep, i)
     assert total.item() == 20 * refs[-1].double().sum().item()
+
+
+def test_conv_sweep_concurrent_exact():
+    """paper_2110_03901_b200.sweep.conv_sweep: independent convolutions in flight together
+    (IMCONV_FLAG_INDEPENDENT on sms // jobs CTAs each, the first launch IMCONV_FLAG_BARRIER).
+    A conv queued just BEFORE the sweep writes the input of the sweep's third member -- the
+    barrier head must keep that member from running ahead of it -- and every output must equal
+    a serialised launch, for several values of jobs."""
+    P = _P()
+    from paper_2110_03901_b200._kernels import conv_device
+    from paper_2110_03901_b200.core import ConvSpec
+    from paper_2110_03901_b200.sweep import conv_sweep
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(21)
+    sq = ConvSpec.square
+    specs = [sq(32, 8, 224, 64, 7, stride=2, pad=3), sq(64, 64, 56, 64, 3, stride=1, pad=1),
+             sq(64, 256, 56, 64, 1), sq(64, 128, 28, 128, 3, stride=1, pad=1), sq(128, 512, 7, 512, 3, stride=1, pad=1),
+             sq(64, 256, 14, 1024, 1), sq(16, 1024, 14, 512, 1)]
+    xs = [torch.randint(-2, 3, (sp.n, sp.h_i, sp.w_i, sp.c_i), device=dev, generator=g).bfloat16() for sp in specs]
+    ws = [torch.randint(-2, 3, (sp.h_f, sp.w_f, sp.c_i, sp.c_o), device=dev, generator=g).bfloat16() for sp in specs]
+    # producer of sweep member 2's input (a 1x1 conv from another tensor, queued before the sweep)
+    src = torch.randint(-1, 2, (64, 56, 56, 64), device=dev, generator=g).bfloat16()
+    wsrc = torch.randint(-1, 2, (1, 1, 64, 256), device=dev, generator=g).bfloat16()
+    xs[2] = torch.empty((64, 56, 56, 256), device=dev, dtype=torch.bfloat16)
+    ref_x2 = conv_device(src, wsrc, 1, 1, 0, 0, 1, 1)
+    refs = [conv_device(x if i != 2 else ref_x2, w, *sp.conv_args(), out_dtype=torch.float32)
+            for i, (sp, x, w) in enumerate(zip(specs, xs, ws))]
+    torch.cuda.synchronize()
+    ys = [torch.empty_like(r) for r in refs]
+    for jobs in (2, 4, 8):
+        for rep in range(3):
+            xs[2].fill_(float("nan"))
+            for y in ys:
+                y.fill_(float("nan"))
+            conv_device(src, wsrc, 1, 1, 0, 0, 1, 1, y=xs[2])
+            conv_sweep([(x, w, sp.conv_args(), y) for sp, x, w, y in zip(specs, xs, ws, ys)], jobs=jobs)
+            torch.cuda.synchronize()
+            for i, (y, ref) in enumerate(zip(ys, refs)):
+                assert torch.equal(y, ref), (jobs, rep, i)

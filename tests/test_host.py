@@ -224,3 +224,20 @@ def test_synthetic_operands_distributions():
     l5 = baseline_configs()["cfg5"][0]
     xi, wi = __import__("paper_2110_03901_b200.workloads", fromlist=["x"]).synthetic_operands(l5, n=1)
     assert xi.dtype == torch.int8 and int(xi.min()) >= -128
+
+
+def test_sweep_rejects_overlapping_buffers():
+    """sweep._check_disjoint (host code): a sweep output may not overlap any operand or output of
+    another member -- the IMCONV_FLAG_INDEPENDENT contract."""
+    import pytest
+    import torch
+    from paper_2110_03901_b200.sweep import _check_disjoint, default_jobs
+    buf = torch.zeros(4096)
+    a, b, c = buf[:1024], buf[1024:2048], buf[2048:3072]
+    w = torch.zeros(64)
+    _check_disjoint([(a, w, None, b), (a, w, None, c)])          # shared inputs are fine
+    with pytest.raises(ValueError):
+        _check_disjoint([(a, w, None, b), (b, w, None, c)])      # output 0 is input 1
+    with pytest.raises(ValueError):
+        _check_disjoint([(a, w, None, buf[1000:1100]), (c, w, None, b)])  # outputs overlap
+    assert default_jobs(2.2e12) < default_jobs(2.7e11)
