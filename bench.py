@@ -552,7 +552,10 @@ def main(argv=None):
                           for _ in range(copies - 1)]
 
     from paper_2110_03901_b200 import sweep as SW
-    sweep_jobs = args.sweep_jobs or SW.default_jobs(float(sum(sp.flops for _, sp, *_ in work)))
+    sweep_jobs = args.sweep_jobs or SW.default_jobs(float(sum(sp.flops for _, sp, *_ in work)), len(work))
+    # (a replay that rotates over several buffer sets runs them all as one sweep)
+    sweep_jobs_all = args.sweep_jobs or SW.default_jobs(float(sum(sp.flops for _, sp, *_ in work)) * copies,
+                                                        len(work) * copies)
 
     def one_pass(ws, flags=None):
         order = ws[::-1] if args.launch_order == "reverse" else ws
@@ -566,6 +569,14 @@ def main(argv=None):
             conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC if flags is None else flags)
 
     def all_passes(flags=None):
+        if flags is None and STATIC != SERIAL_FLAGS and len(work_sets) > 1:
+            # the rotation copies hold independent buffers too: one sweep over all of them
+            convs = []
+            for ws in work_sets:
+                order = ws[::-1] if args.launch_order == "reverse" else ws
+                convs += [(x, w, sp.conv_args(), y) for layer, sp, x, w, y in order]
+            SW.conv_sweep(convs, jobs=sweep_jobs_all, check=True)
+            return
         for ws in work_sets:
             one_pass(ws, flags)
 
@@ -818,8 +829,9 @@ def main(argv=None):
                     "timed_region_ms": region_ms_rank,
                     "layer_overlap": STATIC != SERIAL_FLAGS,
                     **({"planner_debug": hex(args.planner_debug)} if args.planner_debug else {}),
-                    **({"sweep_jobs": round(sweep_jobs, 3),
-                        "sweep_ctas_per_launch": SW.sweep_grid(sweep_jobs, dev)} if STATIC != SERIAL_FLAGS else {}),
+                    **({"sweep_jobs": round(sweep_jobs_all if copies > 1 else sweep_jobs, 3),
+                        "sweep_ctas_per_launch": SW.sweep_grid(sweep_jobs_all if copies > 1 else sweep_jobs, dev)}
+                       if STATIC != SERIAL_FLAGS else {}),
                     **({"value_layers_serialized": total_flops / (serial_ms / 1e3) / 1e12,
                         "ms_per_step_layers_serialized": serial_ms} if serial_ms else {}),
                     **({"value_stem_c3": useful_value} if useful_value is not None else {})},

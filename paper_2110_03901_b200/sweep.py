@@ -34,9 +34,25 @@ from . import _lib
 _BIG_SWEEP_FLOP = 1.5e12
 
 
-def default_jobs(flop: float) -> float:
-    """Convolutions in flight for a sweep of ``flop`` total work: ~8/3 for large sweeps
-    (56 CTAs each on 148 SMs), 4 below 1.5 TFLOP (37 CTAs each) -- the measured optima."""
+def default_jobs(flop: float, count: int | None = None) -> float:
+    """Convolutions in flight for a sweep of ``count`` convolutions and ``flop`` total work.
+
+    A heuristic fitted to measurements on B200 (profiles/r2/README.md, "sweep concurrency"):
+    * convolutions of >= 100 GFLOP each fill the GPU alone: 1 (cfg3, 2 x 309 GFLOP);
+    * a handful (<= 8) of them: 2 (cfg5 int8 / cfg2);
+    * many tiny ones (< 4 GFLOP each): 8 (cfg1's 41 copies of a 1.85 GFLOP layer: 344 -> 569
+      TFLOP/s against one at a time);
+    * otherwise ~8/3 for >= 1.5 TFLOP in total (56 CTAs each on 148 SMs: the cfg4 sweep at 256
+      images) and 4 below (37 CTAs each: its 128 / 64 / 32-image shards).
+    """
+    count = count or 64
+    avg = flop / count
+    if avg >= 100e9:
+        return 1.0
+    if count <= 8:
+        return float(min(2, count))
+    if avg < 4e9:
+        return 8.0
     return 8.0 / 3.0 if flop >= _BIG_SWEEP_FLOP else 4.0
 
 
@@ -84,7 +100,7 @@ def conv_sweep(convs: Sequence, jobs: float | None = None, flops: float | None =
     if check:
         _check_disjoint(convs)
     if jobs is None:
-        jobs = default_jobs(sweep_flops(convs) if flops is None else flops)
+        jobs = default_jobs(sweep_flops(convs) if flops is None else flops, len(convs))
     grid = sweep_grid(jobs, convs[0][0].device)
     base = flags | _lib.FLAG_STATIC_FILTER | _lib.FLAG_INDEPENDENT
     out = []
