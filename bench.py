@@ -480,7 +480,7 @@ def main(argv=None):
     ap.add_argument("--sweep-jobs", type=float, default=0.0,
                     help="convolutions in flight in the overlapped step (paper_2110_03901_b200.sweep; "
                          "0 = the library default for the step's work)")
-    ap.add_argument("--launch-order", default="sweep", choices=["sweep", "reverse"],
+    ap.add_argument("--launch-order", default="sweep", choices=["sweep", "lpt", "reverse"],
                     help="order of the layers' launches inside the timed step (diagnostic)")
     ap.add_argument("--planner-debug", type=lambda v: int(v, 0), default=0,
                     help="diagnostic A/B only: host planner switches (imconv_debug_set_flags bits 16+); "
@@ -563,7 +563,7 @@ def main(argv=None):
             # the overlapped step: the layers as one sweep of independent convolutions, about
             # `sweep_jobs` of them in flight at a time (paper_2110_03901_b200.sweep)
             SW.conv_sweep([(x, w, sp.conv_args(), y) for layer, sp, x, w, y in order], jobs=sweep_jobs,
-                          check=True)
+                          check=True, order="lpt" if args.launch_order == "lpt" else "given")
             return
         for layer, sp, x, w, y in order:
             conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC if flags is None else flags)
@@ -575,7 +575,8 @@ def main(argv=None):
             for ws in work_sets:
                 order = ws[::-1] if args.launch_order == "reverse" else ws
                 convs += [(x, w, sp.conv_args(), y) for layer, sp, x, w, y in order]
-            SW.conv_sweep(convs, jobs=sweep_jobs_all, check=True)
+            SW.conv_sweep(convs, jobs=sweep_jobs_all, check=True,
+                          order="lpt" if args.launch_order == "lpt" else "given")
             return
         for ws in work_sets:
             one_pass(ws, flags)
