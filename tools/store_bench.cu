@@ -107,6 +107,24 @@ int main() {
         const double bytes = static_cast<double>(M) * K * 2;
         printf("%-36s %8.2f us  %6.2f TB/s\n", v.name, best * 1e3, bytes / (best * 1e-3) / 1e12);
     }
+    // per-SM ceiling: the same TMA store stream (2 tiles in flight) from fewer CTAs
+    for (int nb : {2, 0})
+    for (int ctas : {37, 56, 74, 148}) {
+        float best = 1e9f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaMemsetAsync(scrub, rep, scrub_bytes);
+            cudaEventRecord(e0);
+            store_stream<<<ctas, 128, 9 * kTile>>>(tm, nb ? 0 : 1, nb ? nb : 1, M, K, y);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0 && ms < best) best = ms;
+        }
+        const double bytes = static_cast<double>(M) * K * 2;
+        printf("%s %d, %3d CTAs     %8.2f us  %6.2f TB/s  %5.1f GB/s per SM\n", nb ? "TMA store, in flight" : "st.global.v4 (128 thr)", nb, ctas, best * 1e3,
+               bytes / (best * 1e-3) / 1e12, bytes / (best * 1e-3) / 1e9 / ctas);
+    }
     cudaError_t err = cudaDeviceSynchronize();
     printf("status: %s\n", cudaGetErrorString(err));
     return 0;
