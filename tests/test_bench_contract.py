@@ -67,3 +67,30 @@ def test_workload_config_cfg4():
         assert c["global_batch"] == 256 and c["per_gpu_batch"] == per and c["layers"] == 53
         assert c["l2"].startswith("inputs larger than L2")
     assert bench.rotation_copies(baseline_configs()["cfg1"], 1) > 1
+
+
+def test_gpu_arm_json_line():
+    """The GPU arm on the B200 (cfg1, short): one JSON line with every key of the driver
+    contract, the roofline / cpu_baseline / e2e / clocks objects, parity ok on the benchmarked
+    outputs, kernel launches counted, the sweep and the serialised step both timed."""
+    import pytest
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    d = _run(["--config", "cfg1", "--steps", "3", "--warmup", "3", "--no-traffic", "--cpu-sample", "1"])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "gpu_launches", "clocks", "parity"):
+        assert key in d, key
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["gpu_launches"] > 0
+    for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert key in d["roofline"], key
+    assert 0 < d["roofline"]["frac"] < 1.5
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["parity"]["ok"] is True and d["parity"]["checked_images"] > 0
+    assert d["run"]["layer_overlap"] is True and d["run"]["value_layers_serialized"] > 0
+    assert "sm_mhz" in d["clocks"]
+
+
+test_gpu_arm_json_line = __import__("pytest").mark.gpu(test_gpu_arm_json_line)
