@@ -1039,7 +1039,7 @@ __global__ void __launch_bounds__(kThreadsGeneric, 1)
                         ptx::mbar_arrive(&tempty[acc]);
                 }
             } else {
-                // ---- split-K unit (always its CTA's FIRST unit, see get_unit) ----
+                // ---- split-K unit (always its CTA's FIRST unit, see UnitWalk) ----
                 // The tile's output blocks (block b = mt * (BN / kOC) + j: m-tile mt, kOC-column
                 // chunk j) are owned round-robin by the splits (owner = b % S).  Each split writes
                 // the raw 32-bit partial sums of the blocks it does NOT own to the workspace,

@@ -37,17 +37,17 @@ constexpr int kDbgNoTiledA = 1 << 16;     // 1x1 stride-1 layers keep the im2col
 constexpr int kDbgNoBResident = 1 << 17;  // never load the filter slice once per CTA
 constexpr int kDbgNoPdl = 1 << 18;        // launch without programmatic stream serialization
 constexpr int kDbgNoSplitK = 1 << 19;     // never split the tail wave's k-loops
+constexpr int kDbgPlanePitch128 = 1 << 20;  // row-band planes at a 128-byte-multiple pitch (A/B)
 constexpr int kDbgNoAutoPair = 1 << 21;   // never pick CTA pairs automatically
 constexpr int kDbgNoRowPairs = 1 << 22;   // row-band kernel: no N = 128 MMAs over two output rows
 constexpr int kDbgNoStemSpec = 1 << 23;   // row-band kernel: no compile-time stem instantiation
+constexpr int kDbgThrNoPair = 1 << 24;    // throughput mode: sub-wave layers keep single CTAs
 constexpr int kDbgNoHaloStack = 1 << 25;  // halo kernel: one sub-block per block (no shared N = 128 taps)
 constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep the generic kernel
 constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-stationary layout
 constexpr int kDbgNoPairSplit = 1 << 28;  // CTA pairs never split the tail wave's k-loops
-constexpr int kDbgThrNoPair = 1 << 24;    // throughput mode: sub-wave layers keep single CTAs
-constexpr int kDbgPlanePitch128 = 1 << 20;  // row-band planes at a 128-byte-multiple pitch (A/B)
-constexpr int kDbgStreamK = 1 << 29;
-constexpr int kDbgHaloStreamSingle = 1 << 30;  // halo-stream K = 128 layers keep single CTAs (A/B of the pair)      // stream-K the last two waves (measured slower: opt-in, see below)
+constexpr int kDbgStreamK = 1 << 29;      // stream-K the last two waves (measured slower: opt-in, see plan_generic_bn)
+constexpr int kDbgHaloStreamSingle = 1 << 30;  // halo-stream K = 128 layers keep single CTAs (A/B of the pair)
 
 // Split-K ticket counters (conv_kernel.cuh sk_arrive): one per tail tile, never
 // cleared (they only grow, in steps that leave a multiple of kSkRound between
@@ -916,7 +916,7 @@ int plan_generic_bn(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, in
         // output, fence, peer wait, read back) costs ~5-7k cycles per split.  Below one wave
         // it is exposed, so only long k-loops gain (3x3 with C >= 256: 36+ stages).  Behind
         // full waves the split units run first and the exchange hides behind the CTA's next
-        // whole tile (get_unit): k-loops of >= 24 stages gain (tools/ab_layers.py: s5 3x3 at
+        // whole tile (UnitWalk): k-loops of >= 24 stages gain (tools/ab_layers.py: s5 3x3 at
         // N = 256 49.6 -> 41.1 us, s5 1x1a (32 stages) 26.0 -> 23.9; 16-stage 1x1 layers lose ~8%).
         constexpr int kSkMaxSplit = 5, kSkMinStages = 36, kSkMinStagesHidden = 24;
         // Throughput mode (IMCONV_FLAG_INDEPENDENT): a layer's idle SMs -- below one wave or in its
