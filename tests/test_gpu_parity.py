@@ -595,6 +595,49 @@ def test_halo_stream_exact(rng, case):
     assert torch.equal(P._kernels.conv2d_nhwc(xb, wb, *args), y.bfloat16())
 
 
+@pytest.mark.parametrize("case", [
+    # (N, H, C, K, pad, dil): at least one wave of blocks (>= 148), so CTA pairs run two blocks each
+    (64, 28, 128, 128, 1, 1),    # ResNet s3 3x3 shard shape: 256 blocks
+    (151, 14, 256, 128, 1, 1),   # 151 blocks: the last pair's second CTA has no block of its own
+    (75, 20, 128, 128, 2, 2),    # dilation, 2 blocks per image
+])
+def test_halo_stream_pairs_exact(rng, case):
+    """Streamed-filter halo tiles on CTA pairs (K = 128, >= one wave of blocks; an explicit
+    148-CTA grid keeps the halo-stream kernel where the planner's wave rule would pick the generic
+    one): exact against the oracle on the first / middle / last images, equal to the single-CTA
+    kernel (planner switch) and to the generic kernel."""
+    P = _P()
+    import ctypes
+    from oracle import oracle as O
+    from paper_2110_03901_b200._kernels import conv_device
+    from paper_2110_03901_b200.core import ConvSpec
+    from paper_2110_03901_b200.traffic import _args
+    n, h, c, k, pad, dil = case
+    sp = ConvSpec.square(n, c, h, k, 3, stride=1, pad=pad, dilation=dil)
+    a = _args(sp, "bf16", "f32", "reuse_aware", 0)
+    a.num_ctas = 148
+    info = P._lib.ImconvPlanInfo()
+    assert P._lib.lib.imconv_plan(ctypes.byref(a), 148, ctypes.byref(info)) == 0 and info.kernel == 3, case
+    args = sp.conv_args()
+    x = rng.integers(-2, 3, size=(n, h, h, c)).astype(np.int8)
+    w = rng.integers(-2, 3, size=(3, 3, c, k)).astype(np.int8)
+    xb = torch.from_numpy(x).cuda().float().bfloat16()
+    wb = torch.from_numpy(w).cuda().float().bfloat16()
+    y = conv_device(xb, wb, *args, out_dtype=torch.float32, num_ctas=148)
+    imgs = sorted({0, n // 2, n - 2, n - 1})
+    want = O.conv2d_nhwc_exact_f64(x[imgs], w, *args).astype(np.float32)
+    assert np.array_equal(y[imgs].cpu().numpy(), want), case
+    P._lib.lib.imconv_debug_set_flags(1 << 30)  # kDbgHaloStreamSingle
+    try:
+        y_single = conv_device(xb, wb, *args, out_dtype=torch.float32, num_ctas=148)
+    finally:
+        P._lib.lib.imconv_debug_set_flags(0)
+    assert torch.equal(y, y_single)
+    y_generic = conv_device(xb, wb, *args, out_dtype=torch.float32, flags=P._lib.FLAG_NO_HALO)
+    assert torch.equal(y, y_generic)
+    assert torch.equal(conv_device(xb, wb, *args, num_ctas=148), y.bfloat16())
+
+
 def test_static_filter_dependent_chain():
     """IMCONV_FLAG_STATIC_FILTER: the filter loads start before the programmatic-launch wait.
     A chain of dependent convs through every kernel family (row-band stem, stacked halo, generic
