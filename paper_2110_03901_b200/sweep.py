@@ -69,6 +69,10 @@ def _span(t: torch.Tensor):
 
 
 def _check_disjoint(convs) -> None:
+    for i, (x, w, _args, y) in enumerate(convs):
+        for what, t in (("x", x), ("w", w), ("y", y)):
+            if not t.is_contiguous():
+                raise ValueError(f"sweep convolution {i}: {what} must be contiguous (a copy would serialise the sweep)")
     spans = []
     for i, (x, w, _args, y) in enumerate(convs):
         spans.append((i, "x", _span(x)))

@@ -240,5 +240,7 @@ def test_sweep_rejects_overlapping_buffers():
         _check_disjoint([(a, w, None, b), (b, w, None, c)])      # output 0 is input 1
     with pytest.raises(ValueError):
         _check_disjoint([(a, w, None, buf[1000:1100]), (c, w, None, b)])  # outputs overlap
+    with pytest.raises(ValueError):
+        _check_disjoint([(buf.view(64, 64).t(), w, None, b)])          # non-contiguous operand
     assert default_jobs(2.2e12, 53) < default_jobs(2.7e11, 53)
     assert default_jobs(2 * 309e9, 2) == 1.0 and default_jobs(76e9, 41) == 8.0 and default_jobs(266e9, 6) == 2.0
