@@ -47,7 +47,7 @@ constexpr int kDbgNoHaloStream = 1 << 26; // multi-chunk stride-1 layers keep th
 constexpr int kDbgNo1x1Stream = 1 << 27;  // output-heavy 1x1 layers keep the B-stationary layout
 constexpr int kDbgNoPairSplit = 1 << 28;  // CTA pairs never split the tail wave's k-loops
 constexpr int kDbgStreamK = 1 << 29;      // stream-K the last two waves (measured slower: opt-in, see plan_generic_bn)
-constexpr int kDbgHaloStreamSingle = 1 << 30;  // halo-stream K = 128 layers keep single CTAs (A/B of the pair)
+constexpr int kDbgHaloStreamSingle = 1 << 30;  // halo and halo-stream kernels keep single CTAs (A/B of the pairs)
 
 // Split-K ticket counters (conv_kernel.cuh sk_arrive): one per tail tile, never
 // cleared (they only grow, in steps that leave a multiple of kSkRound between
@@ -288,14 +288,14 @@ int launch_rowband(const CUtensorMap &tw, const CUtensorMap &ty, const RowbandPa
 
 constexpr int kNotApplicable = -1000;  // internal: layer does not qualify for a specialised path
 
-template <int ELEM, int OUT, int BN, int HB = 1>
-int launch_halo(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const HaloParams &p, int smem,
-                int grid, cudaStream_t st) {
-    auto kern = conv_halo_kernel<ELEM, OUT, BN, HB>;
+template <int ELEM, int OUT, int BN, int HB = 1, int CG = 1>
+int launch_halo(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ty, const CUtensorMap &tb64,
+                const HaloParams &p, int smem, int grid, cudaStream_t st) {
+    auto kern = conv_halo_kernel<ELEM, OUT, BN, HB, CG>;
     static std::atomic<unsigned long long> attr_done{0};
-    const cudaError_t attr_err = ensure_attrs(attr_done, kern, kMaxDynSmem, false);
+    const cudaError_t attr_err = ensure_attrs(attr_done, kern, kMaxDynSmem, CG == 2);
     if (attr_err != cudaSuccess) return static_cast<int>(attr_err);
-    cudaError_t le = launch_pdl(kern, grid, kThreadsGeneric, smem, st, 1, ta, tb, ty, p);
+    cudaError_t le = launch_pdl(kern, grid, kThreadsGeneric, smem, st, CG, ta, tb, ty, tb64, p);
     if (le != cudaSuccess) return static_cast<int>(le);
     ++g_launches;
     cudaError_t e = cudaGetLastError();
@@ -343,6 +343,20 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
     const int rows_read = std::max(p.tr * p.qp, (hb - 1) * p.tpr * p.qp + 128 + (R - 1) * p.dh * p.qp + (S - 1) * p.dw);
     p.a_stage_bytes = (rows_read * 128 + 1023) / 1024 * 1024;
     p.b_bytes = R * S * K * 128;
+    // stacked bf16/fp16 BN = 64 blocks run on CTA pairs once there is a wave of blocks: each CTA
+    // holds the shared taps' filter rows for one sub-block and 32 of the 64 columns of every tap
+    // (conv_halo.cuh, CG = 2)
+    const int dr_pair = (hb == 2 && p.tpr % p.dh == 0 && p.tpr / p.dh < R) ? p.tpr / p.dh : 0;
+    const int cg = (hb == 2 && E == 2 && p.tiles >= sms && !(a->flags & IMCONV_FLAG_SINGLE_CTA) &&
+                    !(g_debug_flags & kDbgHaloStreamSingle) && (a->num_ctas <= 0 || a->num_ctas % 2 == 0))
+                       ? 2
+                       : 1;
+    if (cg == 2) {
+        p.pair_dr = dr_pair;
+        // shared-tap atoms first (8 KB each, so the SW64 region stays aligned); none without shared taps
+        p.b_single_off = dr_pair > 0 ? (R - dr_pair) * S * K * 128 : 0;
+        p.b_bytes = p.b_single_off + R * S * K * 64;
+    }
     const int kOutTiles = 2 * kBM * 128;
     const int fixed = p.b_bytes + kOutTiles + 1024 /*align*/ + 1024 /*barriers*/;
     if (p.b_bytes > 120 * 1024) return kNotApplicable;
@@ -351,11 +365,22 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
     const int smem = fixed + p.n_stages * p.a_stage_bytes;
 
     if (dry) return 0;  // imconv_plan: applicable, nothing encoded or launched
-    CUtensorMap ta, tb, ty;
+    CUtensorMap ta, tb, ty, tb64;
     std::memset(&ta, 0, sizeof(ta));
     std::memset(&tb, 0, sizeof(tb));
     std::memset(&ty, 0, sizeof(ty));
+    std::memset(&tb64, 0, sizeof(tb64));
     const int64_t N = a->n, H = a->h, W = a->w_, C = a->c;
+    if (cg == 2) {  // half-column (32 x 64 rows, SW64) boxes of the filter for the pair's single taps
+        cuuint64_t gdim[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(R * S * C)};
+        cuuint64_t gstride[1] = {static_cast<cuuint64_t>(K * E)};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(K / 2), static_cast<cuuint32_t>(nc)};
+        cuuint32_t es[2] = {1, 1};
+        if (g_encode_tiled(&tb64, tmap_dtype(a->in_dtype), 2, const_cast<void *>(a->w), gdim, gstride, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return IMCONV_ETMAP;
+    }
     {
         cuuint64_t gdim[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                               static_cast<cuuint64_t>(N)};
@@ -400,14 +425,19 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
             return IMCONV_ETMAP;
     }
     int grid = a->num_ctas > 0 ? a->num_ctas : sms;
-    if (grid > p.tiles) grid = static_cast<int>(p.tiles);
-#define IMCONV_HALO(EL, OUTK)                                                             \
-    switch (K) {                                                                          \
-        case 64:                                                                          \
-            if (hb == 2) return launch_halo<EL, OUTK, 64, 2>(ta, tb, ty, p, smem, grid, st); \
-            return launch_halo<EL, OUTK, 64>(ta, tb, ty, p, smem, grid, st);              \
-        case 128: return launch_halo<EL, OUTK, 128>(ta, tb, ty, p, smem, grid, st);       \
-        default: return launch_halo<EL, OUTK, 256>(ta, tb, ty, p, smem, grid, st);        \
+    if (cg == 2) {  // one pair per two blocks, whole clusters
+        grid = static_cast<int>(std::min<long long>(grid, 2 * ((p.tiles + 1) / 2))) & ~1;
+    } else if (grid > p.tiles) {
+        grid = static_cast<int>(p.tiles);
+    }
+#define IMCONV_HALO(EL, OUTK)                                                                           \
+    switch (K) {                                                                                        \
+        case 64:                                                                                        \
+            if (cg == 2) return launch_halo<EL, OUTK, 64, 2, 2>(ta, tb, ty, tb64, p, smem, grid, st);    \
+            if (hb == 2) return launch_halo<EL, OUTK, 64, 2>(ta, tb, ty, tb64, p, smem, grid, st);       \
+            return launch_halo<EL, OUTK, 64>(ta, tb, ty, tb64, p, smem, grid, st);                      \
+        case 128: return launch_halo<EL, OUTK, 128>(ta, tb, ty, tb64, p, smem, grid, st);               \
+        default: return launch_halo<EL, OUTK, 256>(ta, tb, ty, tb64, p, smem, grid, st);                \
     }
     const bool f32 = a->out_dtype == IMCONV_F32;
     switch (a->in_dtype) {
@@ -416,8 +446,8 @@ int try_halo(const imconv_conv_args *a, int64_t P, int64_t Q, int sms, cudaStrea
         case IMCONV_F16:
             if (f32) { IMCONV_HALO(ELEM_F16, OUT_F32) } else { IMCONV_HALO(ELEM_F16, OUT_F16) }
         case IMCONV_I8:
-            if (K == 128) return launch_halo<ELEM_I8, OUT_I32, 128>(ta, tb, ty, p, smem, grid, st);
-            return launch_halo<ELEM_I8, OUT_I32, 256>(ta, tb, ty, p, smem, grid, st);
+            if (K == 128) return launch_halo<ELEM_I8, OUT_I32, 128>(ta, tb, ty, tb64, p, smem, grid, st);
+            return launch_halo<ELEM_I8, OUT_I32, 256>(ta, tb, ty, tb64, p, smem, grid, st);
         default: return kNotApplicable;
     }
 #undef IMCONV_HALO

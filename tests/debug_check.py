@@ -37,6 +37,7 @@ def cases():
         ("channel-last baseline", sq(2, 64, 12, 64, 3, stride=2, pad=1), bf, 64, 0),
         ("7x7 stem (C = 8)", sq(4, 8, 224, 64, 7, stride=2, pad=3), bf, 0, 0),
         ("3x3 C=64 halo tiles", sq(8, 64, 56, 64, 3, stride=1, pad=1), bf, 0, 0),
+        ("3x3 C=64 halo tiles, CTA pairs", sq(64, 64, 56, 64, 3, stride=1, pad=1), bf, 0, 0),
         ("3x3 C=128 streamed-filter halo", sq(64, 128, 28, 128, 3, stride=1, pad=1), bf, 0, 0),
         ("int8 3x3, CTA pairs", sq(64, 256, 28, 256, 3, stride=1, pad=1), i8, 0, 0),
         ("int8 3x3, CTA pairs + split tail", sq(128, 1024, 7, 1024, 3, stride=1, pad=1), i8, 0, 0),

@@ -638,6 +638,41 @@ def test_halo_stream_pairs_exact(rng, case):
     assert torch.equal(conv_device(xb, wb, *args, num_ctas=148), y.bfloat16())
 
 
+@pytest.mark.parametrize("case", [
+    # (N, H, pad, dil): C = K = 64 stacked halo blocks with >= one wave of blocks -> CTA pairs
+    (64, 56, 1, 1),    # ResNet s2 3x3 shard: shared taps (dr = 2) and single taps
+    (151, 14, 1, 1),   # one block per image (no shared taps), odd block count: a dead second CTA
+    (40, 30, 2, 2),    # dilation
+])
+def test_halo_pairs_exact(rng, case):
+    """Stacked halo tiles on CTA pairs (M = 256; each CTA holds one sub-block's shared-tap filter
+    atoms and 32 of the 64 columns of every tap): exact against the oracle, equal to the single-CTA
+    kernel (planner switch) and to the generic kernel."""
+    P = _P()
+    from oracle import oracle as O
+    from paper_2110_03901_b200._kernels import conv_device
+    from paper_2110_03901_b200.core import ConvSpec
+    n, h, pad, dil = case
+    sp = ConvSpec.square(n, 64, h, 64, 3, stride=1, pad=pad, dilation=dil)
+    args = sp.conv_args()
+    x = rng.integers(-2, 3, size=(n, h, h, 64)).astype(np.int8)
+    w = rng.integers(-2, 3, size=(3, 3, 64, 64)).astype(np.int8)
+    xb = torch.from_numpy(x).cuda().float().bfloat16()
+    wb = torch.from_numpy(w).cuda().float().bfloat16()
+    y = conv_device(xb, wb, *args, out_dtype=torch.float32, num_ctas=148)
+    imgs = sorted({0, n // 2, n - 2, n - 1})
+    want = O.conv2d_nhwc_exact_f64(x[imgs], w, *args).astype(np.float32)
+    assert np.array_equal(y[imgs].cpu().numpy(), want), case
+    P._lib.lib.imconv_debug_set_flags(1 << 30)  # kDbgHaloStreamSingle: halo kernels on single CTAs
+    try:
+        y_single = conv_device(xb, wb, *args, out_dtype=torch.float32, num_ctas=148)
+    finally:
+        P._lib.lib.imconv_debug_set_flags(0)
+    assert torch.equal(y, y_single)
+    assert torch.equal(y, conv_device(xb, wb, *args, out_dtype=torch.float32, flags=P._lib.FLAG_NO_HALO))
+    assert torch.equal(conv_device(xb, wb, *args, num_ctas=148), y.bfloat16())
+
+
 def test_static_filter_dependent_chain():
     """IMCONV_FLAG_STATIC_FILTER: the filter loads start before the programmatic-launch wait.
     A chain of dependent convs through every kernel family (row-band stem, stacked halo, generic
