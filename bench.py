@@ -480,7 +480,7 @@ def main(argv=None):
     ap.add_argument("--sweep-jobs", type=float, default=0.0,
                     help="convolutions in flight in the overlapped step (paper_2110_03901_b200.sweep; "
                          "0 = the library default for the step's work)")
-    ap.add_argument("--launch-order", default="sweep", choices=["sweep", "lpt", "reverse"],
+    ap.add_argument("--launch-order", default="mix", choices=["sweep", "lpt", "reverse", "mix"],
                     help="order of the layers' launches inside the timed step (diagnostic)")
     ap.add_argument("--planner-debug", type=lambda v: int(v, 0), default=0,
                     help="diagnostic A/B only: host planner switches (imconv_debug_set_flags bits 16+); "
@@ -563,7 +563,7 @@ def main(argv=None):
             # the overlapped step: the layers as one sweep of independent convolutions, about
             # `sweep_jobs` of them in flight at a time (paper_2110_03901_b200.sweep)
             SW.conv_sweep([(x, w, sp.conv_args(), y) for layer, sp, x, w, y in order], jobs=sweep_jobs,
-                          check=True, order="lpt" if args.launch_order == "lpt" else "given")
+                          check=True, order=args.launch_order if args.launch_order in ("lpt", "mix") else "given")
             return
         for layer, sp, x, w, y in order:
             conv_device(x, w, *sp.conv_args(), y=y, flags=STATIC if flags is None else flags)
@@ -576,7 +576,7 @@ def main(argv=None):
                 order = ws[::-1] if args.launch_order == "reverse" else ws
                 convs += [(x, w, sp.conv_args(), y) for layer, sp, x, w, y in order]
             SW.conv_sweep(convs, jobs=sweep_jobs_all, check=True,
-                          order="lpt" if args.launch_order == "lpt" else "given")
+                          order=args.launch_order if args.launch_order in ("lpt", "mix") else "given")
             return
         for ws in work_sets:
             one_pass(ws, flags)
@@ -831,7 +831,8 @@ def main(argv=None):
                     "layer_overlap": STATIC != SERIAL_FLAGS,
                     **({"planner_debug": hex(args.planner_debug)} if args.planner_debug else {}),
                     **({"sweep_jobs": round(sweep_jobs_all if copies > 1 else sweep_jobs, 3),
-                        "sweep_ctas_per_launch": SW.sweep_grid(sweep_jobs_all if copies > 1 else sweep_jobs, dev)}
+                        "sweep_ctas_per_launch": SW.sweep_grid(sweep_jobs_all if copies > 1 else sweep_jobs, dev),
+                        "sweep_launch_order": args.launch_order}
                        if STATIC != SERIAL_FLAGS else {}),
                     **({"value_layers_serialized": total_flops / (serial_ms / 1e3) / 1e12,
                         "ms_per_step_layers_serialized": serial_ms} if serial_ms else {}),

@@ -89,13 +89,54 @@ def _check_disjoint(convs) -> None:
                     raise ValueError(f"sweep outputs {i} and {j} overlap")
 
 
-def _est_us(x, w, y) -> float:
-    """Roofline time estimate of one convolution (measured B200 peaks: 1650 TFLOP/s bf16 /
-    3000 TOPS int8, 6500 GB/s): max(tensor time, time to move its operands and output)."""
+def _est_us2(x, w, y) -> tuple:
+    """(tensor time, memory time) of one convolution in us at the measured B200 peaks
+    (1650 TFLOP/s bf16 / 3000 TOPS int8, 6500 GB/s)."""
     flop = 2.0 * y.numel() * w.shape[0] * w.shape[1] * w.shape[2]
     peak = 3000e12 if x.dtype == torch.int8 else 1650e12
     nbytes = x.numel() * x.element_size() + w.numel() * w.element_size() + y.numel() * y.element_size()
-    return max(flop / peak, nbytes / 6500e9) * 1e6
+    return flop / peak * 1e6, nbytes / 6500e9 * 1e6
+
+
+def _est_us(x, w, y) -> float:
+    """Roofline time estimate of one convolution: max(tensor time, time to move its operands
+    and output)."""
+    return max(_est_us2(x, w, y))
+
+
+def mixed_order(convs: Sequence) -> list:
+    """Launch order that keeps the mix of memory and tensor work in flight balanced: with
+    ~jobs launches in flight, a memory-bound layer then runs beside compute-bound ones instead
+    of beside other memory-bound layers.  (A memory-bound layer on a third of the SMs is limited
+    by the per-SM store rate, ~52 GB/s (tools/store_bench.cu), not by HBM, so it costs fewer
+    SM-microseconds there than alone on every SM -- provided the others in flight leave it the
+    HBM bandwidth.)
+
+    The convolutions whose memory share m / (m + t) exceeds the sweep's are merged with the
+    others so that the running surplus of memory time stays near zero; each side goes from its
+    most extreme member to its most balanced one, except that long poles (estimate >= twice the
+    median) lead their side, so the sweep does not end on one long launch."""
+    est = [_est_us2(x, w, y) for x, w, _a, y in convs]
+    goal = sum(m for _t, m in est) / max(sum(t + m for t, m in est), 1e-30)
+    tot = sorted(max(e) for e in est)
+    long_pole = 2.0 * tot[len(tot) // 2]
+    surplus = [m - goal * (t + m) for t, m in est]   # > 0: more memory time than the sweep's mix
+    share = [m / max(t + m, 1e-30) for t, m in est]
+    heavy = sorted((i for i in range(len(est)) if surplus[i] > 0),
+                   key=lambda i: (max(est[i]) < long_pole, -share[i], i))
+    light = sorted((i for i in range(len(est)) if surplus[i] <= 0),
+                   key=lambda i: (max(est[i]) < long_pole, share[i], i))
+    out, a, b, run = [], 0, 0, 0.0
+    while a < len(heavy) or b < len(light):
+        if b >= len(light) or (a < len(heavy) and run <= 0.0):
+            run += surplus[heavy[a]]
+            out.append(heavy[a])
+            a += 1
+        else:
+            run += surplus[light[b]]
+            out.append(light[b])
+            b += 1
+    return out
 
 
 def conv_sweep(convs: Sequence, jobs: float | None = None, flops: float | None = None,
@@ -117,13 +158,18 @@ def conv_sweep(convs: Sequence, jobs: float | None = None, flops: float | None =
         jobs = default_jobs(sweep_flops(convs) if flops is None else flops, len(convs))
     grid = sweep_grid(jobs, convs[0][0].device)
     base = flags | _lib.FLAG_STATIC_FILTER | _lib.FLAG_INDEPENDENT
-    # launch order: "given" = as listed (default), "lpt" = longest estimated first; outputs are
-    # returned as listed.  On the cfg4 sweep the given ResNet order, which alternates memory- and
-    # compute-bound layers, measured best at 256 images (909-920 vs lpt 899-902 TFLOP/s; 32-image
-    # shard 6505 vs 6548; reverse order 851 / 5800)
+    # launch order: "given" = as listed (default), "lpt" = longest estimated first, "mix" =
+    # memory and tensor work balanced (mixed_order); outputs are returned as listed.  On the cfg4
+    # sweep at 256 images: given (ResNet order, which already alternates memory- and compute-bound
+    # layers) 925-928 TFLOP/s, mix 929-936, lpt 899-902 against given 909-920 on another box,
+    # reverse 851; 32-image shard x 8: given 6448-6488, mix 6526-6594.  Per-launch grids snapped
+    # to whole waves (e.g. 50 instead of 56 CTAs for the 98 pair blocks of a stage-5 layer)
+    # measured no gain: the SMs a short last wave leaves idle already run the next launch.
     idx = list(range(len(convs)))
     if order == "lpt":
         idx.sort(key=lambda i: -_est_us(convs[i][0], convs[i][1], convs[i][3]))
+    elif order == "mix":
+        idx = mixed_order(convs)
     elif order != "given":
         raise ValueError(f"unknown sweep order {order!r}")
     out = [None] * len(convs)

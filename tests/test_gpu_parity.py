@@ -799,7 +799,9 @@ def test_conv_sweep_concurrent_exact():
             for y in ys:
                 y.fill_(float("nan"))
             conv_device(src, wsrc, 1, 1, 0, 0, 1, 1, y=xs[2])
-            conv_sweep([(x, w, sp.conv_args(), y) for sp, x, w, y in zip(specs, xs, ws, ys)], jobs=jobs)
+            # (the barrier head is the first LAUNCH whatever the order puts there)
+            conv_sweep([(x, w, sp.conv_args(), y) for sp, x, w, y in zip(specs, xs, ws, ys)], jobs=jobs,
+                       order=("given", "mix", "lpt")[rep])
             torch.cuda.synchronize()
             for i, (y, ref) in enumerate(zip(ys, refs)):
                 assert torch.equal(y, ref), (jobs, rep, i)

@@ -226,6 +226,44 @@ def test_synthetic_operands_distributions():
     assert xi.dtype == torch.int8 and int(xi.min()) >= -128
 
 
+def test_sweep_mixed_order_balances_memory_and_tensor_work():
+    """sweep.mixed_order (host code): a permutation of the sweep in which memory-bound and
+    compute-bound convolutions alternate (bounded running surplus of memory time), and the
+    long-pole stem is launched early."""
+    import torch
+    from paper_2110_03901_b200 import sweep as SW
+    from paper_2110_03901_b200.workloads import baseline_configs
+    layers = baseline_configs()["cfg4"]
+    convs = []
+    for l in layers:
+        sp = l.spec
+        convs.append((torch.empty((sp.n, sp.h_i, sp.w_i, sp.c_i), dtype=torch.bfloat16, device="meta"),
+                      torch.empty((sp.h_f, sp.w_f, sp.c_i, sp.c_o), dtype=torch.bfloat16, device="meta"),
+                      sp.conv_args(),
+                      torch.empty((sp.n, sp.h_o, sp.w_o, sp.c_o), dtype=torch.bfloat16, device="meta")))
+    order = SW.mixed_order(convs)
+    assert sorted(order) == list(range(len(convs)))
+    est = [SW._est_us2(x, w, y) for x, w, _a, y in convs]
+    goal = sum(m for _t, m in est) / sum(t + m for t, m in est)
+    # the running surplus of memory time over the sweep's mix never exceeds one layer's worth,
+    # where the ResNet order accumulates several stage-2 layers' worth
+    surplus = [est[i][1] - goal * sum(est[i]) for i in range(len(convs))]
+    bound = max(abs(v) for v in surplus) + 1e-9
+
+    def worst(seq):
+        run, w = 0.0, 0.0
+        for i in seq:
+            run += surplus[i]
+            w = max(w, abs(run))
+        return w
+
+    assert worst(order) <= bound
+    assert worst(range(len(convs))) > 3 * bound
+    assert [layers[i].name for i in order].index("stem") < 4
+    # one-sided sweeps keep their order
+    assert SW.mixed_order(convs[1:2] * 3) == [0, 1, 2]
+
+
 def test_sweep_rejects_overlapping_buffers():
     """sweep._check_disjoint (host code): a sweep output may not overlap any operand or output of
     another member -- the IMCONV_FLAG_INDEPENDENT contract."""
