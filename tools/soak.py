@@ -4,7 +4,7 @@ launch mode the sweep and the bench use -- default, IMCONV_FLAG_INDEPENDENT on 5
 forced CTA pairs / single CTAs, no-halo -- integer-valued bf16 with fp32 output and int8, all
 bit-exact against the oracle.  Prints the first mismatch and exits 1.
 
-  python tools/soak.py [--seeds 40] [--start 5000]
+  python tools/soak.py [--seeds 40] [--start 5000] [--debug-build]
 """
 import argparse
 import os
@@ -22,10 +22,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seeds", type=int, default=40)
     ap.add_argument("--start", type=int, default=5000)
+    ap.add_argument("--debug-build", action="store_true",
+                    help="run through libimconv_debug.so (device invariant checks: mbarrier phases, tickets, ...)")
     args = ap.parse_args()
     import torch
     import paper_2110_03901_b200 as P
     from paper_2110_03901_b200 import _lib
+    if args.debug_build:
+        _lib.use_debug()
     from paper_2110_03901_b200._kernels import conv_device
     from oracle import oracle as O
     from test_gpu_fuzz import _random_case
